@@ -1,0 +1,226 @@
+"""ctypes bindings for the TEST-ONLY oracle libraries.
+
+* ``oracle/lib/libvt_oracle.so`` -- the C restatement of the reference scalar
+  codec (oracle/vt_oracle.c), always available after ``make -C oracle``.
+* ``oracle/_ref/libvtrans_ref.so`` -- the unmodified reference library compiled
+  out of tree (oracle/Makefile); present where /root/reference was available
+  at build time (and shipped to the GPU box with the snapshot).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg import
+this module.  The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "lib", "libvt_oracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libvtrans_ref.so")
+
+
+class CRes(C.Structure):
+    _fields_ = [("consumed", C.c_uint64), ("written", C.c_uint64), ("error_at", C.c_int64)]
+
+
+@dataclass(frozen=True)
+class Result:
+    """Python view of vtrans::TranscodeResult (error_at None == empty optional)."""
+
+    consumed: int
+    written: int
+    error_at: int | None
+
+    @staticmethod
+    def of(c: CRes) -> "Result":
+        return Result(int(c.consumed), int(c.written), None if c.error_at < 0 else int(c.error_at))
+
+
+_u8p = C.POINTER(C.c_uint8)
+_u16p = C.POINTER(C.c_uint16)
+
+
+def _p8(a):
+    return a.ctypes.data_as(_u8p)
+
+
+def _p16(a):
+    return a.ctypes.data_as(_u16p)
+
+
+def ensure_built() -> None:
+    if not os.path.exists(ORACLE_SO):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=True)
+
+
+class _Lib:
+    def __init__(self, path: str, prefix: str):
+        self.lib = C.CDLL(path)
+        self.prefix = prefix
+
+    def fn(self, name, res, *args):
+        f = getattr(self.lib, self.prefix + name)
+        f.restype = res
+        f.argtypes = list(args)
+        return f
+
+
+class Oracle:
+    """The C restatement (vt_oracle.c)."""
+
+    def __init__(self):
+        ensure_built()
+        L = _Lib(ORACLE_SO, "vto_")
+        self._u8to16 = L.fn("utf8_to_utf16", None, _u8p, C.c_uint64, _u16p, C.POINTER(CRes))
+        self._u16to8 = L.fn("utf16_to_utf8", None, _u16p, C.c_uint64, _u8p, C.POINTER(CRes))
+        self._u8to16mt = L.fn("utf8_to_utf16_mt", None, _u8p, C.c_uint64, _u16p, C.c_int, C.POINTER(CRes))
+        self._u16to8mt = L.fn("utf16_to_utf8_mt", None, _u16p, C.c_uint64, _u8p, C.c_int, C.POINTER(CRes))
+        self._v8 = L.fn("validate_utf8", C.c_int64, _u8p, C.c_uint64)
+        self._v16 = L.fn("validate_utf16", C.c_int64, _u16p, C.c_uint64)
+        self._c8 = L.fn("count_utf8", C.c_int64, _u8p, C.c_uint64)
+        self._c16 = L.fn("count_utf16", C.c_int64, _u16p, C.c_uint64)
+        self._exh = L.fn("exhaustive_short_verdicts", C.c_uint64, _u8p)
+        self._enc8 = L.fn("encode_utf8", C.c_uint32, C.c_uint32, _u8p)
+        self._enc16 = L.fn("encode_utf16", C.c_uint32, C.c_uint32, _u16p)
+
+    def utf8_to_utf16(self, data, threads: int = 1):
+        a = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+        a = np.ascontiguousarray(a, dtype=np.uint8)
+        out = np.zeros(len(a) + 8, dtype=np.uint16)
+        r = CRes()
+        if threads > 1:
+            self._u8to16mt(_p8(a), len(a), _p16(out), threads, C.byref(r))
+        else:
+            self._u8to16(_p8(a), len(a), _p16(out), C.byref(r))
+        res = Result.of(r)
+        return out[: res.written].copy(), res
+
+    def utf16_to_utf8(self, units, threads: int = 1):
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        out = np.zeros(3 * len(a) + 16, dtype=np.uint8)
+        r = CRes()
+        if threads > 1:
+            self._u16to8mt(_p16(a), len(a), _p8(out), threads, C.byref(r))
+        else:
+            self._u16to8(_p16(a), len(a), _p8(out), C.byref(r))
+        res = Result.of(r)
+        return out[: res.written].copy(), res
+
+    def validate_utf8(self, data) -> int | None:
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)
+        e = self._v8(_p8(a), len(a))
+        return None if e < 0 else int(e)
+
+    def validate_utf16(self, units) -> int | None:
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        e = self._v16(_p16(a), len(a))
+        return None if e < 0 else int(e)
+
+    def count_utf8(self, data) -> int | None:
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)
+        c = self._c8(_p8(a), len(a))
+        return None if c < 0 else int(c)
+
+    def count_utf16(self, units) -> int | None:
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        c = self._c16(_p16(a), len(a))
+        return None if c < 0 else int(c)
+
+    def exhaustive_short_verdicts(self) -> np.ndarray:
+        out = np.zeros(256 + 65536 + 16777216, dtype=np.uint8)
+        k = self._exh(_p8(out))
+        assert k == len(out)
+        return out
+
+    def encode_utf8(self, cp: int) -> bytes:
+        b = np.zeros(4, dtype=np.uint8)
+        k = self._enc8(cp, _p8(b))
+        return bytes(b[:k])
+
+    def encode_utf16(self, cp: int) -> list[int]:
+        u = np.zeros(2, dtype=np.uint16)
+        k = self._enc16(cp, _p16(u))
+        return [int(x) for x in u[:k]]
+
+
+class Reference:
+    """The unmodified reference library (oracle/_ref/libvtrans_ref.so)."""
+
+    @staticmethod
+    def available() -> bool:
+        return os.path.exists(REF_SO)
+
+    def __init__(self):
+        L = _Lib(REF_SO, "vtr_")
+        self._u8to16 = L.fn("utf8_to_utf16", None, _u8p, C.c_uint64, _u16p, C.c_int, C.POINTER(CRes))
+        self._u16to8 = L.fn("utf16_to_utf8", None, _u16p, C.c_uint64, _u8p, C.POINTER(CRes))
+        self._s8to16 = L.fn("scalar_utf8_to_utf16", None, _u8p, C.c_uint64, _u16p, C.POINTER(CRes))
+        self._s16to8 = L.fn("scalar_utf16_to_utf8", None, _u16p, C.c_uint64, _u8p, C.POINTER(CRes))
+        self._v8 = L.fn("validate_utf8", C.c_int, _u8p, C.c_uint64)
+        self._v16 = L.fn("validate_utf16", C.c_int64, _u16p, C.c_uint64)
+        self._c8 = L.fn("count_utf8", C.c_int64, _u8p, C.c_uint64)
+        self._c16 = L.fn("count_utf16", C.c_int64, _u16p, C.c_uint64)
+        self._exh = L.fn("exhaustive_short_verdicts", C.c_uint64, _u8p)
+        self._u8to16mt = L.fn("utf8_to_utf16_mt", None, _u8p, C.c_uint64, _u16p, C.c_int, C.POINTER(CRes))
+        self._u16to8mt = L.fn("utf16_to_utf8_mt", None, _u16p, C.c_uint64, _u8p, C.c_int, C.POINTER(CRes))
+        self._v8mt = L.fn("validate_utf8_mt", C.c_int, _u8p, C.c_uint64, C.c_int)
+        self.native = bool(L.fn("native_backend", C.c_int)())
+
+    def utf8_to_utf16(self, data, validate=True, scalar=False, threads=1, out=None):
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)
+        if out is None:
+            out = np.zeros(len(a) + 8, dtype=np.uint16)
+        r = CRes()
+        if scalar:
+            self._s8to16(_p8(a), len(a), _p16(out), C.byref(r))
+        elif threads > 1:
+            self._u8to16mt(_p8(a), len(a), _p16(out), threads, C.byref(r))
+        else:
+            self._u8to16(_p8(a), len(a), _p16(out), int(validate), C.byref(r))
+        res = Result.of(r)
+        return out[: res.written], res
+
+    def utf16_to_utf8(self, units, scalar=False, threads=1, out=None):
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        if out is None:
+            out = np.zeros(3 * len(a) + 16, dtype=np.uint8)
+        r = CRes()
+        if scalar:
+            self._s16to8(_p16(a), len(a), _p8(out), C.byref(r))
+        elif threads > 1:
+            self._u16to8mt(_p16(a), len(a), _p8(out), threads, C.byref(r))
+        else:
+            self._u16to8(_p16(a), len(a), _p8(out), C.byref(r))
+        res = Result.of(r)
+        return out[: res.written], res
+
+    def validate_utf8(self, data, threads=1) -> bool:
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)
+        if threads > 1:
+            return bool(self._v8mt(_p8(a), len(a), threads))
+        return bool(self._v8(_p8(a), len(a)))
+
+    def validate_utf16(self, units) -> int | None:
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        e = self._v16(_p16(a), len(a))
+        return None if e < 0 else int(e)
+
+    def count_utf8(self, data) -> int | None:
+        a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)
+        c = self._c8(_p8(a), len(a))
+        return None if c < 0 else int(c)
+
+    def count_utf16(self, units) -> int | None:
+        a = np.ascontiguousarray(np.asarray(units, dtype=np.uint16))
+        c = self._c16(_p16(a), len(a))
+        return None if c < 0 else int(c)
+
+    def exhaustive_short_verdicts(self) -> np.ndarray:
+        out = np.zeros(256 + 65536 + 16777216, dtype=np.uint8)
+        k = self._exh(_p8(out))
+        assert k == len(out)
+        return out
