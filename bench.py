@@ -1,0 +1,380 @@
+"""Benchmark of the validated UTF-8 -> UTF-16LE hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+Workload (BASELINE.json configs[1], "cfg2"): 1 GiB of valid UTF-8, CJK-heavy
+(75% U+4E00-9FFF, 20% ASCII events with runs, 5% U+0080-07FF), seeded and
+generated directly in HBM (synthetic stand-in for the paper's corpora).  A
+step is one validating transcode of the whole input through the device-pointer
+C ABI (vt_utf8_to_utf16_async) -- one kernel launch.  The input (1 GiB) is
+larger than the 126 MB L2, so no flush is needed between steps.
+
+Metric: input GB/s (aggregate over GPUs) with Gchar/s and the HBM roofline
+fraction beside it.  Multi-GPU (torchrun, one process per GPU): weak scaling,
+each rank transcodes its own 1 GiB slice of the stream (disjoint chunk ranges);
+no data-path collective, timing is the max over ranks.
+
+``--impl reference`` times the reference's own CPU implementation (the
+unmodified library compiled out of tree into oracle/_ref, SIMD path, on
+character-boundary shards over all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: ("cfg1: UTF-8->UTF-16LE validating, 16 MiB, 90% U+0020-007E / 10% U+0080-07FF", 16 << 20, "utf8"),
+    2: ("cfg2: UTF-8->UTF-16LE validating, 1 GiB, 75% U+4E00-9FFF / 20% ASCII (runs) / 5% U+0080-07FF",
+        1 << 30, "utf8"),
+    3: ("cfg3: UTF-16LE->UTF-8, 1 GiB UTF-16, 60/15/15/10% 1/2/3/4-byte classes", 1 << 29, "utf16"),
+    4: ("cfg4: UTF-8->UTF-16LE validating, 1 GiB, 25/25/25/25% + ~1 error per 64 MiB", 1 << 30, "utf8"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU works."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        busy = [r for r in self.rows if r[2].isdigit() and int(r[2]) > 0] or self.rows
+        sm = [int(r[0]) for r in busy if r[0].isdigit()]
+        mx = [int(r[1]) for r in self.rows if r[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(busy)}
+
+
+def cpu_baseline_run(host_in, threads: int, reps: int, kind_pref: str = "reference"):
+    """Times the reference CPU path (oracle/_ref, all host threads) -- or the
+    oracle port when the reference build is missing -- on host_in."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+
+    from oracle_lib import Oracle, Reference
+
+    if Reference.available():
+        ref, kind = Reference(), "reference"
+        run = lambda: ref.utf8_to_utf16(host_in, threads=threads, out=out)
+    else:
+        orc, kind = Oracle(), "port"
+        run = lambda: orc.utf8_to_utf16(host_in, threads=threads)
+    out = np.empty(len(host_in) + 8, dtype=np.uint16)
+    best = None
+    res = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, res = run()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, kind, res
+
+
+def run_reference_arm(args, rank: int):
+    """--impl reference: the reference's own CPU implementation on this box."""
+    import numpy as np
+
+    import paper_2109_10433_b200 as vt
+
+    if rank != 0:
+        return None
+    desc, size, kind = CONFIGS[args.config]
+    # input on the host via the host-side generator (no GPU involved)
+    draws = int(vt.lib().vt_gen_chunk_draws(args.config))
+    chunks = []
+    total = 0
+    c = 0
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        while total < size:
+            batch = list(ex.map(lambda k: vt.generate_host_chunk(args.config, args.config, k)[0],
+                                range(c, c + 256)))
+            c += 256
+            for a in batch:
+                chunks.append(a)
+                total += len(a)
+                if total >= size:
+                    break
+    host = np.concatenate(chunks)
+    n = size
+    while n > 0 and (host[n] & 0xC0) == 0x80:
+        n -= 1  # cut at a character boundary
+    host = np.ascontiguousarray(host[:n])
+    threads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference
+
+    out = np.empty(n + 8, dtype=np.uint16)
+    if Reference.available():
+        impl, ck = Reference(), "reference"
+        step = lambda: impl.utf8_to_utf16(host, threads=threads, out=out)
+    else:
+        impl, ck = Oracle(), "port"
+        step = lambda: impl.utf8_to_utf16(host, threads=threads)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, r = step()
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    gbs = n / t / 1e9
+    return {
+        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)", "value": round(gbs, 4), "unit": "GB/s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded generator, BASELINE cfg2 shape)",
+        "config": {"workload": desc, "input_bytes": n, "parallelism": f"cpu x{threads} threads"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": ck,
+                         "sample": f"whole cfg{args.config} input ({n} bytes) per step, "
+                                   f"reference SIMD path on {threads} character-boundary shards"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result": {"consumed": r.consumed, "written": r.written, "error_at": r.error_at},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 4])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        line = run_reference_arm(args, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2109_10433_b200 as vt
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc, size, kind = CONFIGS[args.config]
+    # each rank its own slice of the stream: disjoint chunk ranges
+    d_in, n, first_bad = vt.generate(args.config, size, chunk0=rank * 1_000_000)
+    torch.cuda.synchronize()
+    d_out = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+    d_res = torch.zeros(3, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        vt.utf8_to_utf16_device(d_in, n, d_out, stream=stream, d_res=d_res)
+
+    with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        # keep the GPU busy long enough for nvidia-smi to see the load
+        t_end = time.time() + 0.6
+        while time.time() < t_end:
+            step()
+            torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = vt.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches = vt.launch_count() - launches0
+        if dist:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+    res = vt.result_from_device(d_res)
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        # combine the per-rank results (3 integers per rank; shards are independent)
+        from paper_2109_10433_b200 import TranscodeResult, sharding
+
+        mine = torch.tensor([res.consumed, res.written, -1 if res.error_at is None else res.error_at],
+                            device="cuda")
+        allr = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(world)]
+        dist.all_gather(allr, mine)
+        ns = torch.tensor([n], device="cuda")
+        alln = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+        dist.all_gather(alln, ns)
+        starts = np.concatenate([[0], np.cumsum([int(x.item()) for x in alln])]).tolist()
+        rs = [TranscodeResult(int(x[0]), int(x[1]), None if int(x[2]) < 0 else int(x[2])) for x in allr]
+        total_n = starts[-1]
+        gres, _ = sharding.combine(starts, rs, total_n)
+    else:
+        total_n = n
+        gres = res
+    per_step_ms = ms_max / args.steps
+    chars = vt.validate_utf8_device(d_in, n).written  # code points of this rank's slice
+    if dist:
+        c = torch.tensor([chars], device="cuda")
+        dist.all_reduce(c)
+        chars = int(c.item())
+    value = total_n / (per_step_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    alg_bytes = n + 2 * res.written  # per launch, this rank
+    achieved = alg_bytes / (ms / args.steps / 1e3) / 1e9
+
+    line = {
+        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(per_step_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (seeded splitmix64 chunk generator in HBM, BASELINE cfg shape; corpora absent)",
+        "config": {"workload": desc, "input_bytes_per_gpu": n, "output_units_per_gpu": res.written,
+                   "chars_total": chars, "l2": "input 1 GiB > 126 MB L2: no flush between steps",
+                   "parallelism": f"shards x{world} (no collective)" if world > 1 else "single GPU"},
+        "gchars_per_s": round(chars / (per_step_ms / 1e3) / 1e9, 2),
+        "result": {"consumed": gres.consumed, "written": gres.written, "error_at": gres.error_at},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "vt::utf8_kernel<true>",
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr):
+        with open(tr) as f:
+            t = json.load(f).get(f"cfg{args.config}")
+        if t:
+            line["roofline"]["traffic"] = t["dram_bytes_per_launch"]
+            line["roofline"]["traffic_source"] = t["source"]
+
+    if rank == 0 and world == 1 and not args.no_e2e:
+        # end to end through the drop-in (host-pointer) C ABI: pinned host input,
+        # H2D + kernel + D2H of result and output inside the timed region
+        h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h_in.copy_(d_in[:n])
+        h_out = torch.empty(n + 8, dtype=torch.int16, pin_memory=True)
+        import ctypes
+
+        L = vt.lib()
+        r = vt._CRes()
+
+        def e2e_step():
+            rc = L.vt_host_utf8_to_utf16(h_in.data_ptr(), n, h_out.data_ptr(), ctypes.byref(r))
+            assert rc == 0
+        for _ in range(2):
+            e2e_step()
+        k = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            e2e_step()
+        dt = (time.perf_counter() - t0) / k
+        assert r.written == res.written and r.error_at == (-1 if res.error_at is None else res.error_at)
+        line["e2e"] = {"value": round(n / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n,
+                       "d2h_bytes_per_step": 2 * int(r.written) + 24,
+                       "api": "vt_host_utf8_to_utf16 (drop-in boundary), pinned host buffers",
+                       "ms_per_step": round(dt * 1e3, 3)}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host = d_in[:n].cpu().numpy()
+        threads = os.cpu_count() or 1
+        t, kind_, cres = cpu_baseline_run(host, threads, reps=3)
+        assert cres.written == res.written and cres.error_at == res.error_at, "CPU baseline disagrees"
+        # the reference's own design point: one thread, on a 64 MiB prefix
+        m = 64 << 20
+        while m > 0 and (host[m] & 0xC0) == 0x80:
+            m -= 1
+        t1, _, _ = cpu_baseline_run(host[:m], 1, reps=2)
+        line["cpu_baseline"] = {
+            "value": round(n / t / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind_,
+            "sample": f"whole cfg{args.config} input ({n} bytes), reference SIMD path (oracle/_ref, "
+                      f"-O3 SSE4.1) on {threads} character-boundary shards, best of 3; "
+                      f"1-thread on a {m}-byte prefix: {m / t1 / 1e9:.3f} GB/s",
+            "single_thread_gbs": round(m / t1 / 1e9, 3),
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/* vtrans_gpu.h -- C ABI of the B200 (sm_100a) transcoding library
+ * libvtrans_gpu.so.
+ *
+ * Plain pointers and sizes; no C++ or torch types.  Every entry point returns
+ * an int status: 0 on success, a CUDA runtime error code (> 0) on a device or
+ * runtime failure, or a negative VT_E* code.  Data errors (invalid UTF-8 /
+ * UTF-16) are never statuses: they are reported in-band through vt_result,
+ * exactly like vtrans::TranscodeResult (proj/include/vtrans/codec_core.hpp:11-21).
+ *
+ * Reference interfaces replaced (paths relative to the reference root):
+ *   vt_host_utf8_to_utf16    vtrans::utf8_to_utf16(span, u16*, bool, PathCounters*)
+ *                            proj/include/vtrans/utf8_to_utf16.hpp:29-30
+ *   vt_host_utf16_to_utf8    vtrans::utf16_to_utf8(span, u8*)
+ *                            proj/include/vtrans/utf16_to_utf8.hpp:15
+ *   vt_host_validate_utf8    vtrans::validate_utf8(span)  proj/include/vtrans/validation.hpp:27
+ *   vt_host_validate_utf16   vtrans::validate_utf16(span) proj/include/vtrans/validation.hpp:31
+ *   vt_host_count_utf8/16    vtrans::scalar::count_codepoints_utf8/16
+ *                            proj/include/vtrans/codec_core.hpp:66-67
+ * The vt_* device-pointer forms are the same operations on device-resident
+ * buffers, enqueued on a caller stream; the bench and the sharder use them.
+ * The vtrans:: C++ drop-in (include/vtrans/*.hpp) is a thin layer over the
+ * vt_host_* entry points.
+ */
+#ifndef VTRANS_GPU_H
+#define VTRANS_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same meaning and layout as the reference's TranscodeResult:
+ * error_at == -1 is the empty optional; when error_at >= 0, consumed ==
+ * error_at and out[0..written) is the exact transcoding of the valid prefix.
+ * For the validate/count entry points `written` is the number of code points
+ * in the valid prefix (== the full count when error_at == -1). */
+typedef struct vt_result {
+  uint64_t consumed;
+  uint64_t written;
+  int64_t error_at;
+} vt_result;
+
+typedef struct CUstream_st* vt_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+#define VT_E_NODEVICE (-1)  /* no CUDA device visible: there is no CPU fallback */
+#define VT_E_ARG (-2)       /* invalid argument */
+#define VT_E_ARCH (-3)      /* device is not sm_100 (the kernels are sm_100a-only) */
+
+/* ---- device-pointer API ------------------------------------------------
+ * Inputs and outputs are device (or host-mapped) pointers.  The *_async forms
+ * enqueue on `stream` and write the result to device memory `d_res`; the plain
+ * forms additionally wait and return the result in host memory `h_res`.
+ * Capacities (the reference's contracts): UTF-8 -> UTF-16 needs >= n units,
+ * UTF-16 -> UTF-8 needs >= 3n + 16 bytes.  Only out[0..written) is defined. */
+int vt_utf8_to_utf16_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
+                           vt_stream stream);
+int vt_utf16_to_utf8_async(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res,
+                           vt_stream stream);
+int vt_validate_utf8_async(const uint8_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream);
+int vt_validate_utf16_async(const uint16_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream);
+
+int vt_utf8_to_utf16(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* h_res,
+                     vt_stream stream);
+int vt_utf16_to_utf8(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* h_res,
+                     vt_stream stream);
+int vt_validate_utf8(const uint8_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream);
+int vt_validate_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream);
+
+/* ---- host-pointer API (the drop-in boundary) ------------------------------
+ * Host buffers in, host buffers out; staging, transfers and the kernels are
+ * handled internally on a per-thread stream.  Thread-safe. */
+int vt_host_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res);
+int vt_host_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, vt_result* res);
+/* first_err: index of the first invalid byte / unit, or -1 when valid. */
+int vt_host_validate_utf8(const uint8_t* in, uint64_t n, int64_t* first_err);
+int vt_host_validate_utf16(const uint16_t* in, uint64_t n, int64_t* first_err);
+/* count: code points, or -1 when the input is invalid (std::nullopt). */
+int vt_host_count_utf8(const uint8_t* in, uint64_t n, int64_t* count);
+int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count);
+
+/* ---- batched short strings ------------------------------------------------
+ * `count` strings back to back in `d_data`; string i is
+ * [d_offsets[i], d_offsets[i+1]).  Writes the first error index or -1. */
+int vt_validate_utf8_batch(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           int64_t* d_first_err, vt_stream stream);
+/* Verdict (1 = valid) of every 1-, 2- and 3-byte input in the enumeration
+ * order of acceptance C3 (proj/tests/acceptance.cpp:147-167);
+ * d_verdicts holds 16843008 bytes. */
+int vt_exhaustive_short_verdicts(uint8_t* d_verdicts, vt_stream stream);
+
+/* ---- multi-GPU sharder ------------------------------------------------------
+ * Splits a host buffer at character boundaries into `ndev` shards (0 = one
+ * per visible GPU; shard k runs on GPU k % count),
+ * runs the single-GPU path per shard concurrently (one host thread per GPU,
+ * no collective), and combines: output offsets by exclusive scan of the
+ * per-shard `written`, error from the first failing shard. */
+int vt_sharded_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, int ndev,
+                             vt_result* res);
+int vt_sharded_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, int ndev,
+                             vt_result* res);
+/* Host-side split-point rules the sharder uses (exposed for tests). */
+uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut);
+uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut);
+
+/* ---- synthetic workloads (BASELINE.json configs 1-5) ----------------------
+ * Deterministic, chunked: chunk c of configuration `cfg` is a function of
+ * (seed, c) only.  vt_gen_sizes writes each chunk's size in bytes (UTF-8) or
+ * units (UTF-16, cfg 3); vt_gen_write writes the chunks at `d_offsets`
+ * (exclusive scan of the sizes), dropping every character that would end past
+ * `limit`, and stores the end of the last whole character below `limit` to
+ * *d_end (device). */
+int vt_gen_sizes(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks, uint64_t* d_sizes,
+                 vt_stream stream);
+int vt_gen_write(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks,
+                 const uint64_t* d_offsets, uint64_t limit, void* d_out, uint64_t* d_end,
+                 vt_stream stream);
+uint64_t vt_gen_chunk_draws(int cfg);
+/* One chunk generated on the host (same definition); returns its size and
+ * writes at most `cap` elements.  *first_bad: offset of the first injected
+ * malformed sequence (cfg 4) or UINT64_MAX. */
+uint64_t vt_gen_host_chunk(int cfg, uint64_t seed, uint64_t chunk, void* out, uint64_t cap,
+                           uint64_t* first_bad);
+
+/* ---- misc ------------------------------------------------------------------- */
+const char* vt_status_string(int status);
+int vt_device_count(void);
+/* Number of kernels this library launched so far in the calling process. */
+uint64_t vt_launch_count(void);
+const char* vt_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VTRANS_GPU_H */

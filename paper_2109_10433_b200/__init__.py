@@ -1,0 +1,364 @@
+"""B200-native validated UTF-8 <-> UTF-16LE transcoding (arXiv 2109.10433 hot path).
+
+Python face of ``libvtrans_gpu.so`` (built in-tree under ``lib/``), bound with
+ctypes to the C ABI declared in ``include/vtrans_gpu.h``.  The host-pointer
+functions mirror the reference's entry points (``vtrans::utf8_to_utf16``,
+``vtrans::utf16_to_utf8``, ``validate_utf8``, ``validate_utf16``, the code-point
+counts) with the same argument meaning, return values and error semantics:
+data errors come back in-band in :class:`TranscodeResult`, device failures
+raise :class:`VtransError`.  There is no CPU implementation in this package: if
+the library or the GPU is missing, calls fail loudly.
+
+The ``*_device`` functions take torch CUDA tensors (device memory and streams
+are torch's plumbing) and call the device-pointer ABI directly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libvtrans_gpu.so")
+
+__all__ = [
+    "TranscodeResult", "VtransError", "lib", "utf8_to_utf16", "utf16_to_utf8", "validate_utf8",
+    "validate_utf16", "count_utf8", "count_utf16", "utf8_to_utf16_device", "utf16_to_utf8_device",
+    "validate_utf8_device", "validate_utf16_device", "validate_utf8_batch",
+    "exhaustive_short_verdicts", "sharded_utf8_to_utf16", "sharded_utf16_to_utf8",
+    "split_point_utf8", "split_point_utf16", "generate", "launch_count", "device_count",
+]
+
+
+class VtransError(RuntimeError):
+    """A device or runtime failure (never a data error)."""
+
+
+class _CRes(C.Structure):
+    _fields_ = [("consumed", C.c_uint64), ("written", C.c_uint64), ("error_at", C.c_int64)]
+
+
+@dataclass(frozen=True)
+class TranscodeResult:
+    """vtrans::TranscodeResult (proj/include/vtrans/codec_core.hpp:14-21)."""
+
+    consumed: int
+    written: int
+    error_at: Optional[int]
+
+    def ok(self) -> bool:
+        return self.error_at is None
+
+    @staticmethod
+    def _of(c: _CRes) -> "TranscodeResult":
+        return TranscodeResult(int(c.consumed), int(c.written),
+                               None if c.error_at < 0 else int(c.error_at))
+
+
+_lib = None
+_u8p, _u16p, _vp = C.POINTER(C.c_uint8), C.POINTER(C.c_uint16), C.c_void_p
+
+
+def lib():
+    """Loads libvtrans_gpu.so (raises VtransError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise VtransError(f"{LIB_PATH} is missing: run `python -m paper_2109_10433_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "vt_utf8_to_utf16_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_utf16_to_utf8_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_validate_utf8_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+        "vt_validate_utf16_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+        "vt_utf8_to_utf16": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes), _vp]),
+        "vt_utf16_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes), _vp]),
+        "vt_validate_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(_CRes), _vp]),
+        "vt_validate_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(_CRes), _vp]),
+        "vt_host_utf8_to_utf16": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes)]),
+        "vt_host_utf16_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes)]),
+        "vt_host_validate_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_host_validate_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_host_count_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_host_count_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_validate_utf8_batch": (C.c_int, [_vp, _vp, C.c_uint64, _vp, _vp]),
+        "vt_exhaustive_short_verdicts": (C.c_int, [_vp, _vp]),
+        "vt_sharded_utf8_to_utf16": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
+        "vt_sharded_utf16_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
+        "vt_split_point_utf8": (C.c_uint64, [_vp, C.c_uint64, C.c_uint64]),
+        "vt_split_point_utf16": (C.c_uint64, [_vp, C.c_uint64, C.c_uint64]),
+        "vt_gen_sizes": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp]),
+        "vt_gen_write": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _vp, C.c_uint64,
+                                   _vp, _vp, _vp]),
+        "vt_gen_chunk_draws": (C.c_uint64, [C.c_int]),
+        "vt_gen_host_chunk": (C.c_uint64, [C.c_int, C.c_uint64, C.c_uint64, _vp, C.c_uint64,
+                                           C.POINTER(C.c_uint64)]),
+        "vt_status_string": (C.c_char_p, [C.c_int]),
+        "vt_device_count": (C.c_int, []),
+        "vt_launch_count": (C.c_uint64, []),
+        "vt_build_info": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise VtransError(f"{what}: {lib().vt_status_string(rc).decode()} (status {rc})")
+
+
+def _bytes_view(data) -> np.ndarray:
+    if isinstance(data, np.ndarray):
+        return np.ascontiguousarray(data.view(np.uint8) if data.dtype != np.uint8 else data)
+    return np.frombuffer(bytes(data), dtype=np.uint8)
+
+
+def _units_view(units) -> np.ndarray:
+    a = np.asarray(units)
+    if a.dtype != np.uint16:
+        a = a.astype(np.uint16)
+    return np.ascontiguousarray(a)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+# ---- host-pointer API (the drop-in boundary) --------------------------------
+
+def utf8_to_utf16(data, validate: bool = True) -> tuple[np.ndarray, TranscodeResult]:
+    """vtrans::utf8_to_utf16 vector overload (proj/include/vtrans/utf8_to_utf16.hpp:32-33).
+
+    ``validate`` is accepted for parity; the GPU always validates (allowed: the
+    reference leaves non-validating output on invalid input unspecified)."""
+    a = _bytes_view(data)
+    out = np.empty(len(a) + 8, dtype=np.uint16)
+    r = _CRes()
+    _check(lib().vt_host_utf8_to_utf16(_ptr(a), len(a), out.ctypes.data, C.byref(r)), "utf8_to_utf16")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def utf16_to_utf8(units) -> tuple[np.ndarray, TranscodeResult]:
+    """vtrans::utf16_to_utf8 vector overload (proj/include/vtrans/utf16_to_utf8.hpp:17)."""
+    a = _units_view(units)
+    out = np.empty(3 * len(a) + 16, dtype=np.uint8)
+    r = _CRes()
+    _check(lib().vt_host_utf16_to_utf8(_ptr(a), len(a), out.ctypes.data, C.byref(r)), "utf16_to_utf8")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def validate_utf8(data) -> bool:
+    """vtrans::validate_utf8 (proj/include/vtrans/validation.hpp:27)."""
+    return first_error_utf8(data) is None
+
+
+def first_error_utf8(data) -> Optional[int]:
+    a = _bytes_view(data)
+    e = C.c_int64()
+    _check(lib().vt_host_validate_utf8(_ptr(a), len(a), C.byref(e)), "validate_utf8")
+    return None if e.value < 0 else int(e.value)
+
+
+def validate_utf16(units) -> Optional[int]:
+    """vtrans::validate_utf16 (proj/include/vtrans/validation.hpp:31)."""
+    a = _units_view(units)
+    e = C.c_int64()
+    _check(lib().vt_host_validate_utf16(_ptr(a), len(a), C.byref(e)), "validate_utf16")
+    return None if e.value < 0 else int(e.value)
+
+
+def count_utf8(data) -> Optional[int]:
+    """Code points, None when invalid (scalar::count_codepoints_utf8 semantics)."""
+    a = _bytes_view(data)
+    c = C.c_int64()
+    _check(lib().vt_host_count_utf8(_ptr(a), len(a), C.byref(c)), "count_utf8")
+    return None if c.value < 0 else int(c.value)
+
+
+def count_utf16(units) -> Optional[int]:
+    a = _units_view(units)
+    c = C.c_int64()
+    _check(lib().vt_host_count_utf16(_ptr(a), len(a), C.byref(c)), "count_utf16")
+    return None if c.value < 0 else int(c.value)
+
+
+# ---- device-pointer API (torch tensors) --------------------------------------
+
+def _stream_ptr(stream) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def utf8_to_utf16_device(d_in, n: int, d_out, stream=None, d_res=None, offset: int = 0):
+    """Transcodes ``n`` bytes at ``d_in.data_ptr() + offset`` into ``d_out``.
+
+    With ``d_res`` (a CUDA tensor of >= 24 bytes) the call is asynchronous and
+    returns None; otherwise it waits and returns the TranscodeResult."""
+    p = d_in.data_ptr() + offset
+    if d_res is not None:
+        _check(lib().vt_utf8_to_utf16_async(p, n, d_out.data_ptr(), d_res.data_ptr(),
+                                            _stream_ptr(stream)), "utf8_to_utf16_async")
+        return None
+    r = _CRes()
+    _check(lib().vt_utf8_to_utf16(p, n, d_out.data_ptr(), C.byref(r), _stream_ptr(stream)),
+           "utf8_to_utf16")
+    return TranscodeResult._of(r)
+
+
+def utf16_to_utf8_device(d_in, n: int, d_out, stream=None, d_res=None, offset: int = 0):
+    """``n`` UTF-16 units at ``d_in.data_ptr() + offset`` (bytes) into ``d_out``."""
+    p = d_in.data_ptr() + offset
+    if d_res is not None:
+        _check(lib().vt_utf16_to_utf8_async(p, n, d_out.data_ptr(), d_res.data_ptr(),
+                                            _stream_ptr(stream)), "utf16_to_utf8_async")
+        return None
+    r = _CRes()
+    _check(lib().vt_utf16_to_utf8(p, n, d_out.data_ptr(), C.byref(r), _stream_ptr(stream)),
+           "utf16_to_utf8")
+    return TranscodeResult._of(r)
+
+
+def validate_utf8_device(d_in, n: int, stream=None, d_res=None, offset: int = 0):
+    p = d_in.data_ptr() + offset
+    if d_res is not None:
+        _check(lib().vt_validate_utf8_async(p, n, d_res.data_ptr(), _stream_ptr(stream)),
+               "validate_utf8_async")
+        return None
+    r = _CRes()
+    _check(lib().vt_validate_utf8(p, n, C.byref(r), _stream_ptr(stream)), "validate_utf8")
+    return TranscodeResult._of(r)
+
+
+def validate_utf16_device(d_in, n: int, stream=None, d_res=None, offset: int = 0):
+    p = d_in.data_ptr() + offset
+    if d_res is not None:
+        _check(lib().vt_validate_utf16_async(p, n, d_res.data_ptr(), _stream_ptr(stream)),
+               "validate_utf16_async")
+        return None
+    r = _CRes()
+    _check(lib().vt_validate_utf16(p, n, C.byref(r), _stream_ptr(stream)), "validate_utf16")
+    return TranscodeResult._of(r)
+
+
+def result_from_device(d_res) -> TranscodeResult:
+    """Decodes a device result slot (an int64 CUDA tensor of 3 elements)."""
+    v = d_res.cpu().numpy().astype(np.int64)
+    return TranscodeResult(int(v[0]), int(v[1]), None if v[2] < 0 else int(v[2]))
+
+
+def validate_utf8_batch(d_data, d_offsets, count: int, d_first_err, stream=None) -> None:
+    _check(lib().vt_validate_utf8_batch(d_data.data_ptr(), d_offsets.data_ptr(), count,
+                                        d_first_err.data_ptr(), _stream_ptr(stream)),
+           "validate_utf8_batch")
+
+
+def exhaustive_short_verdicts(device="cuda"):
+    import torch
+
+    out = torch.empty(256 + 65536 + 16777216, dtype=torch.uint8, device=device)
+    _check(lib().vt_exhaustive_short_verdicts(out.data_ptr(), _stream_ptr(None)),
+           "exhaustive_short_verdicts")
+    return out
+
+
+# ---- multi-GPU sharder ------------------------------------------------------------
+
+def sharded_utf8_to_utf16(data, ndev: int = 0):
+    a = _bytes_view(data)
+    out = np.empty(len(a) + 8, dtype=np.uint16)
+    r = _CRes()
+    _check(lib().vt_sharded_utf8_to_utf16(_ptr(a), len(a), out.ctypes.data, ndev, C.byref(r)),
+           "sharded_utf8_to_utf16")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def sharded_utf16_to_utf8(units, ndev: int = 0):
+    a = _units_view(units)
+    out = np.empty(3 * len(a) + 16, dtype=np.uint8)
+    r = _CRes()
+    _check(lib().vt_sharded_utf16_to_utf8(_ptr(a), len(a), out.ctypes.data, ndev, C.byref(r)),
+           "sharded_utf16_to_utf8")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def split_point_utf8(data, cut: int) -> int:
+    a = _bytes_view(data)
+    return int(lib().vt_split_point_utf8(_ptr(a), len(a), cut))
+
+
+def split_point_utf16(units, cut: int) -> int:
+    a = _units_view(units)
+    return int(lib().vt_split_point_utf16(_ptr(a), len(a), cut))
+
+
+# ---- synthetic workloads ------------------------------------------------------------
+
+def generate(cfg: int, size: int, seed: Optional[int] = None, chunk0: int = 0, device="cuda",
+             stream=None):
+    """Generates configuration ``cfg`` (1-5) of BASELINE.json directly in HBM.
+
+    ``size`` is in bytes for UTF-8 configs and in units for cfg 3 (UTF-16).
+    Returns ``(tensor, n, first_injected)``: a uint8 tensor (UTF-8) or int16
+    tensor (UTF-16 units) holding exactly ``n`` elements of whole characters,
+    n <= size, and for cfg 4 the position of the first injected error (else
+    None)."""
+    import torch
+
+    seed = cfg if seed is None else seed
+    L = lib()
+    draws = int(L.vt_gen_chunk_draws(cfg))
+    per_draw = {1: 1.1, 2: 3.25, 3: 1.1, 4: 2.5, 5: 1.75}[cfg]
+    nchunks = int(size / (draws * per_draw) * 1.08) + 2
+    s = _stream_ptr(stream)
+    while True:
+        sizes = torch.empty(nchunks, dtype=torch.int64, device=device)
+        _check(L.vt_gen_sizes(cfg, seed, chunk0, nchunks, sizes.data_ptr(), s), "gen_sizes")
+        csum = torch.cumsum(sizes, 0)
+        if int(csum[-1]) >= size:
+            break
+        nchunks = nchunks * 2
+    offsets = torch.zeros(nchunks, dtype=torch.int64, device=device)
+    offsets[1:] = csum[:-1]
+    dtype = torch.int16 if cfg == 3 else torch.uint8
+    out = torch.empty(size + 16, dtype=dtype, device=device)
+    end = torch.empty(2, dtype=torch.int64, device=device)
+    _check(L.vt_gen_write(cfg, seed, chunk0, nchunks, offsets.data_ptr(), size, out.data_ptr(),
+                          end.data_ptr(), s), "gen_write")
+    e = end.cpu().numpy().view(np.uint64)
+    n = int(e[0])
+    first_bad = None if int(e[1]) == 0xFFFFFFFFFFFFFFFF else int(e[1])
+    return out, n, first_bad
+
+
+def generate_host_chunk(cfg: int, seed: int, chunk: int) -> tuple[np.ndarray, Optional[int]]:
+    """One chunk generated on the CPU (same definition as the device generator)."""
+    L = lib()
+    cap = int(L.vt_gen_chunk_draws(cfg)) * 64 + 64
+    out = np.empty(cap, dtype=np.uint16 if cfg == 3 else np.uint8)
+    fb = C.c_uint64()
+    k = int(L.vt_gen_host_chunk(cfg, seed, chunk, out.ctypes.data, cap, C.byref(fb)))
+    return out[:k], (None if fb.value == 0xFFFFFFFFFFFFFFFF else int(fb.value))
+
+
+def launch_count() -> int:
+    """Kernels launched by libvtrans_gpu in this process so far."""
+    return int(lib().vt_launch_count())
+
+
+def device_count() -> int:
+    return int(lib().vt_device_count())

@@ -1,0 +1,86 @@
+// k_batch.cu -- many-short-strings validation on sm_100a.
+//
+// The reference is called millions of times on tiny inputs by its fuzzer and
+// exhaustive suites (proj/src/harness.cpp:388-436, proj/tests/acceptance.cpp:
+// 138-204).  A per-call kernel launch would be latency-bound, so these
+// entry points validate a whole batch of strings in one launch: one thread per
+// string walks it with the decode rules of proj/src/codec_core.cpp:5-38 and
+// reports the first failing index.
+#include "vt_device.cuh"
+#include "vt_kernels.h"
+
+namespace vt {
+
+// First error index of bytes [p, p+n), or -1.
+__device__ __forceinline__ long long first_error_seq(const uint8_t* p, unsigned long long n) {
+  unsigned long long i = 0;
+  while (i < n) {
+    const unsigned b0 = p[i];
+    if (b0 < 0x80u) {
+      i++;
+      continue;
+    }
+    unsigned len, cp, lo;
+    if ((b0 & 0xE0u) == 0xC0u) {
+      len = 2; cp = b0 & 0x1Fu; lo = 0x80u;
+    } else if ((b0 & 0xF0u) == 0xE0u) {
+      len = 3; cp = b0 & 0x0Fu; lo = 0x800u;
+    } else if ((b0 & 0xF8u) == 0xF0u) {
+      len = 4; cp = b0 & 0x07u; lo = 0x10000u;
+    } else {
+      return (long long)i;
+    }
+    if (i + len > n) return (long long)i;
+    for (unsigned k = 1; k < len; k++) {
+      const unsigned c = p[i + k];
+      if ((c & 0xC0u) != 0x80u) return (long long)i;
+      cp = (cp << 6) | (c & 0x3Fu);
+    }
+    if (cp < lo || cp > 0x10FFFFu || (cp >= 0xD800u && cp <= 0xDFFFu)) return (long long)i;
+    i += len;
+  }
+  return -1;
+}
+
+__global__ void batch_validate_kernel(const uint8_t* data, const uint64_t* offsets,
+                                      uint64_t count, int64_t* first_err) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t s = offsets[i], e = offsets[i + 1];
+  first_err[i] = first_error_seq(data + s, e - s);
+}
+
+// Input number k of the 1/2/3-byte enumeration (acceptance.cpp:147-167).
+__global__ void exhaustive_short_kernel(uint8_t* verdicts) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= 256u + 65536u + 16777216u) return;
+  uint8_t b[3];
+  unsigned len;
+  uint32_t v;
+  if (k < 256u) {
+    len = 1; v = k;
+  } else if (k < 256u + 65536u) {
+    len = 2; v = k - 256u;
+  } else {
+    len = 3; v = k - 256u - 65536u;
+  }
+  for (unsigned i = 0; i < len; i++) b[i] = (uint8_t)(v >> (8 * (len - 1 - i)));
+  verdicts[k] = first_error_seq(b, len) < 0 ? 1 : 0;
+}
+
+int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                               int64_t* first_err, cudaStream_t s) {
+  if (count == 0) return 0;
+  const unsigned threads = 128;
+  const uint64_t blocks = (count + threads - 1) / threads;
+  batch_validate_kernel<<<(unsigned)blocks, threads, 0, s>>>(data, offsets, count, first_err);
+  return (int)cudaGetLastError();
+}
+
+int launch_exhaustive_short(uint8_t* verdicts, cudaStream_t s) {
+  const unsigned total = 256u + 65536u + 16777216u;
+  exhaustive_short_kernel<<<(total + 255) / 256, 256, 0, s>>>(verdicts);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace vt

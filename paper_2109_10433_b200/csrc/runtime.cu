@@ -1,0 +1,586 @@
+// runtime.cu -- the C ABI of libvtrans_gpu.so (include/vtrans_gpu.h).
+//
+// Owns per-(device, stream) scratch for the single-pass kernels (control block,
+// epoch-tagged tile status array, device result), the per-thread host contexts
+// behind the host-pointer entry points (stream, pinned mapped staging, device
+// buffers), and the multi-GPU sharder.  No entry point computes anything on the
+// CPU: a missing device is an error (VT_E_NODEVICE), never a fallback.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <utility>
+#include <vector>
+
+#include "../../include/vtrans_gpu.h"
+#include "vt_device.cuh"
+#include "vt_kernels.h"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+#define VT_STR2(x) #x
+#define VT_STR(x) VT_STR2(x)
+
+#define VT_TRY(expr)                    \
+  do {                                  \
+    const int rc_ = (int)(expr);        \
+    if (rc_ != 0) return rc_;           \
+  } while (0)
+
+struct DeviceInfo {
+  int sms = 0;
+  int occ_u8[2] = {0, 0};
+  int occ_u16[2] = {0, 0};
+  bool ok = false;
+};
+
+std::mutex g_dev_mu;
+std::map<int, DeviceInfo> g_devs;
+
+int device_info(int dev, DeviceInfo& out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_devs.find(dev);
+  if (it != g_devs.end()) {
+    out = it->second;
+    return 0;
+  }
+  cudaDeviceProp p;
+  VT_TRY(cudaGetDeviceProperties(&p, dev));
+  if (p.major != 10) return VT_E_ARCH;
+  DeviceInfo d;
+  d.sms = p.multiProcessorCount;
+  d.occ_u8[0] = std::max(1, vt::occupancy_utf8(false));
+  d.occ_u8[1] = std::max(1, vt::occupancy_utf8(true));
+  d.occ_u16[0] = std::max(1, vt::occupancy_utf16(false));
+  d.occ_u16[1] = std::max(1, vt::occupancy_utf16(true));
+  d.ok = true;
+  g_devs[dev] = d;
+  out = d;
+  return 0;
+}
+
+int current_device(int& dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return VT_E_NODEVICE;
+  }
+  VT_TRY(cudaGetDevice(&dev));
+  return 0;
+}
+
+// Scratch for the kernels enqueued on one stream of one device.  Calls on the
+// same stream are ordered by the stream, so one scratch serves them all; the
+// mutex only guards the host-side bookkeeping (epoch, growth).
+struct Scratch {
+  std::mutex mu;
+  int dev = -1;
+  vt::Ctl* ctl = nullptr;
+  unsigned long long* status = nullptr;
+  size_t status_cap = 0;  // tiles
+  unsigned epoch = 0;
+  vt_result* d_res = nullptr;  // device result slot for the synchronous API
+  vt_result* h_res = nullptr;  // pinned host mirror
+};
+
+std::mutex g_scratch_mu;
+std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Scratch>> g_scratch;
+
+Scratch* scratch_for(int dev, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  auto& p = g_scratch[{dev, s}];
+  if (!p) {
+    p.reset(new Scratch());
+    p->dev = dev;
+  }
+  return p.get();
+}
+
+// Ensures capacity for `tiles` status words and returns the epoch to use.
+int prepare(Scratch& sc, cudaStream_t s, unsigned tiles, unsigned& epoch) {
+  if (!sc.ctl) {
+    VT_TRY(cudaMalloc(&sc.ctl, sizeof(vt::Ctl)));
+    vt::Ctl init{};
+    init.err = vt::kNoError;
+    VT_TRY(cudaMemcpy(sc.ctl, &init, sizeof init, cudaMemcpyHostToDevice));
+  }
+  if (tiles > sc.status_cap) {
+    VT_TRY(cudaStreamSynchronize(s));  // the old array may still be in use
+    if (sc.status) VT_TRY(cudaFree(sc.status));
+    size_t cap = std::max<size_t>(tiles, 1u << 16);
+    VT_TRY(cudaMalloc(&sc.status, cap * sizeof(unsigned long long)));
+    VT_TRY(cudaMemset(sc.status, 0, cap * sizeof(unsigned long long)));
+    sc.status_cap = cap;
+    sc.epoch = 0;
+  }
+  sc.epoch = (sc.epoch + 1) & 0x3FFF;
+  if (sc.epoch == 0) {
+    // epoch wrapped: clear stale tags so no old status can match a new epoch
+    VT_TRY(cudaMemsetAsync(sc.status, 0, sc.status_cap * sizeof(unsigned long long), s));
+    sc.epoch = 1;
+  }
+  epoch = sc.epoch;
+  return 0;
+}
+
+int grid_for(unsigned tiles, int occ, int sms) {
+  const long long g = (long long)occ * sms;
+  return (int)std::max(1LL, std::min<long long>(tiles, g));
+}
+
+// Enqueues one UTF-8 kernel; the caller holds sc.mu.
+int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint64_t n,
+                    uint16_t* d_out, vt_result* d_res, cudaStream_t s, bool transcode) {
+  if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
+  vt::U8Args a;
+  const uintptr_t p = (uintptr_t)d_in;
+  a.head = p & 15;
+  a.base = reinterpret_cast<const uint8_t*>(p - a.head);
+  a.n = n;
+  a.ntiles = vt::tiles_utf8(a.head, n);
+  VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
+  a.out = d_out;
+  a.status = sc->status;
+  a.ctl = sc->ctl;
+  a.res = d_res;
+  const int grid = grid_for(a.ntiles, di.occ_u8[transcode], di.sms);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_utf8(a, transcode, grid, s);
+}
+
+int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, uint64_t n,
+                     uint8_t* d_out, vt_result* d_res, cudaStream_t s, bool transcode) {
+  if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
+  if (((uintptr_t)d_in & 1) != 0) return VT_E_ARG;
+  vt::U16Args a;
+  const uintptr_t p = (uintptr_t)d_in;
+  a.head = (p & 15) >> 1;
+  a.base = reinterpret_cast<const uint16_t*>(p - (p & 15));
+  a.n = n;
+  a.ntiles = vt::tiles_utf16(a.head, n);
+  VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
+  a.out = d_out;
+  a.status = sc->status;
+  a.ctl = sc->ctl;
+  a.res = d_res;
+  const int grid = grid_for(a.ntiles, di.occ_u16[transcode], di.sms);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_utf16(a, transcode, grid, s);
+}
+
+struct Target {
+  Scratch* sc;
+  DeviceInfo di;
+};
+
+int target(cudaStream_t s, Target& t) {
+  int dev;
+  VT_TRY(current_device(dev));
+  VT_TRY(device_info(dev, t.di));
+  t.sc = scratch_for(dev, s);
+  return 0;
+}
+
+int run_utf8(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res, cudaStream_t s,
+             bool transcode) {
+  Target t;
+  VT_TRY(target(s, t));
+  std::lock_guard<std::mutex> lk(t.sc->mu);
+  return run_utf8_locked(t.sc, t.di, d_in, n, d_out, d_res, s, transcode);
+}
+
+int run_utf16(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res, cudaStream_t s,
+              bool transcode) {
+  Target t;
+  VT_TRY(target(s, t));
+  std::lock_guard<std::mutex> lk(t.sc->mu);
+  return run_utf16_locked(t.sc, t.di, d_in, n, d_out, d_res, s, transcode);
+}
+
+// Enqueues through `enqueue(scratch, devinfo, d_res)` and returns the result to
+// host memory.  The scratch lock is held throughout, so the scratch's result
+// slots are never shared between concurrent callers of one stream.
+template <class F>
+int sync_result(cudaStream_t s, vt_result* h_res, F&& enqueue) {
+  if (!h_res) return VT_E_ARG;
+  Target t;
+  VT_TRY(target(s, t));
+  Scratch* sc = t.sc;
+  std::lock_guard<std::mutex> lk(sc->mu);
+  if (!sc->d_res) {
+    VT_TRY(cudaMalloc(&sc->d_res, sizeof(vt_result)));
+    VT_TRY(cudaMallocHost(&sc->h_res, sizeof(vt_result)));
+  }
+  VT_TRY(enqueue(sc, t.di, sc->d_res));
+  VT_TRY(cudaMemcpyAsync(sc->h_res, sc->d_res, sizeof(vt_result), cudaMemcpyDeviceToHost, s));
+  VT_TRY(cudaStreamSynchronize(s));
+  *h_res = *sc->h_res;
+  return 0;
+}
+
+// ---- per-thread host contexts for the host-pointer API -----------------------
+constexpr uint64_t kZeroCopyMax = 64 * 1024;  // bytes of input
+
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  uint8_t* h_in = nullptr;   // pinned, mapped
+  uint8_t* h_out = nullptr;  // pinned, mapped
+  vt_result* h_res = nullptr;
+  vt_result* d_res = nullptr;
+  uint8_t* d_in = nullptr;
+  uint8_t* d_out = nullptr;
+  size_t d_in_cap = 0, d_out_cap = 0;
+  ~HostCtx() {
+    // process teardown: the driver reclaims everything; avoid CUDA calls here
+  }
+};
+
+thread_local std::map<int, HostCtx> t_ctx;
+
+int host_ctx(HostCtx*& out) {
+  int dev;
+  VT_TRY(current_device(dev));
+  DeviceInfo di;
+  VT_TRY(device_info(dev, di));
+  HostCtx& c = t_ctx[dev];
+  if (!c.stream) {
+    VT_TRY(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    VT_TRY(cudaHostAlloc(&c.h_in, kZeroCopyMax + 64, cudaHostAllocMapped));
+    VT_TRY(cudaHostAlloc(&c.h_out, 3 * kZeroCopyMax + 64, cudaHostAllocMapped));
+    VT_TRY(cudaHostAlloc(&c.h_res, sizeof(vt_result), cudaHostAllocMapped));
+    VT_TRY(cudaMalloc(&c.d_res, sizeof(vt_result)));
+    c.dev = dev;
+  }
+  out = &c;
+  return 0;
+}
+
+int ensure_dev(uint8_t*& p, size_t& cap, size_t need, cudaStream_t s) {
+  if (need <= cap) return 0;
+  VT_TRY(cudaStreamSynchronize(s));
+  if (p) VT_TRY(cudaFree(p));
+  size_t c = std::max(need + need / 4, (size_t)1 << 20);
+  VT_TRY(cudaMalloc(&p, c));
+  cap = c;
+  return 0;
+}
+
+template <class In, class Out, class Run>
+int host_transcode(const In* in, uint64_t n, Out* out, uint64_t out_cap_elems, vt_result* res,
+                   Run run) {
+  if (!res || (n && (!in || !out))) return VT_E_ARG;
+  HostCtx* c;
+  VT_TRY(host_ctx(c));
+  const size_t in_bytes = n * sizeof(In);
+  if (in_bytes <= kZeroCopyMax) {
+    // one launch, no copies: the kernel reads and writes mapped pinned memory
+    if (n) std::memcpy(c->h_in, in, in_bytes);
+    In* din;
+    Out* dout;
+    vt_result* dres;
+    VT_TRY(cudaHostGetDevicePointer((void**)&din, c->h_in, 0));
+    VT_TRY(cudaHostGetDevicePointer((void**)&dout, c->h_out, 0));
+    VT_TRY(cudaHostGetDevicePointer((void**)&dres, c->h_res, 0));
+    VT_TRY(run(din, n, dout, dres, c->stream));
+    VT_TRY(cudaStreamSynchronize(c->stream));
+    *res = *c->h_res;
+    if (res->written > out_cap_elems) return VT_E_ARG;
+    if (res->written) std::memcpy(out, c->h_out, res->written * sizeof(Out));
+    return 0;
+  }
+  VT_TRY(ensure_dev(c->d_in, c->d_in_cap, in_bytes, c->stream));
+  VT_TRY(ensure_dev(c->d_out, c->d_out_cap, out_cap_elems * sizeof(Out) + 16, c->stream));
+  VT_TRY(cudaMemcpyAsync(c->d_in, in, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  VT_TRY(run(reinterpret_cast<const In*>(c->d_in), n, reinterpret_cast<Out*>(c->d_out), c->d_res,
+             c->stream));
+  VT_TRY(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(vt_result), cudaMemcpyDeviceToHost, c->stream));
+  VT_TRY(cudaStreamSynchronize(c->stream));
+  *res = *c->h_res;
+  if (res->written > out_cap_elems) return VT_E_ARG;
+  if (res->written)
+    VT_TRY(cudaMemcpyAsync(out, c->d_out, res->written * sizeof(Out), cudaMemcpyDeviceToHost,
+                           c->stream));
+  VT_TRY(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+template <class In, class Run>
+int host_validate(const In* in, uint64_t n, vt_result* res, Run run) {
+  if (!res || (n && !in)) return VT_E_ARG;
+  HostCtx* c;
+  VT_TRY(host_ctx(c));
+  const size_t in_bytes = n * sizeof(In);
+  if (in_bytes <= kZeroCopyMax) {
+    if (n) std::memcpy(c->h_in, in, in_bytes);
+    In* din;
+    vt_result* dres;
+    VT_TRY(cudaHostGetDevicePointer((void**)&din, c->h_in, 0));
+    VT_TRY(cudaHostGetDevicePointer((void**)&dres, c->h_res, 0));
+    VT_TRY(run(din, n, dres, c->stream));
+    VT_TRY(cudaStreamSynchronize(c->stream));
+    *res = *c->h_res;
+    return 0;
+  }
+  VT_TRY(ensure_dev(c->d_in, c->d_in_cap, in_bytes, c->stream));
+  VT_TRY(cudaMemcpyAsync(c->d_in, in, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  VT_TRY(run(reinterpret_cast<const In*>(c->d_in), n, c->d_res, c->stream));
+  VT_TRY(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(vt_result), cudaMemcpyDeviceToHost, c->stream));
+  VT_TRY(cudaStreamSynchronize(c->stream));
+  *res = *c->h_res;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vt_utf8_to_utf16_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
+                           vt_stream stream) {
+  return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, true);
+}
+
+int vt_utf16_to_utf8_async(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res,
+                           vt_stream stream) {
+  return run_utf16(d_in, n, d_out, d_res, (cudaStream_t)stream, true);
+}
+
+int vt_validate_utf8_async(const uint8_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream) {
+  return run_utf8(d_in, n, nullptr, d_res, (cudaStream_t)stream, false);
+}
+
+int vt_validate_utf16_async(const uint16_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream) {
+  return run_utf16(d_in, n, nullptr, d_res, (cudaStream_t)stream, false);
+}
+
+int vt_utf8_to_utf16(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* h_res,
+                     vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf8_locked(sc, di, d_in, n, d_out, d, s, true);
+  });
+}
+
+int vt_utf16_to_utf8(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* h_res,
+                     vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf16_locked(sc, di, d_in, n, d_out, d, s, true);
+  });
+}
+
+int vt_validate_utf8(const uint8_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf8_locked(sc, di, d_in, n, nullptr, d, s, false);
+  });
+}
+
+int vt_validate_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf16_locked(sc, di, d_in, n, nullptr, d, s, false);
+  });
+}
+
+int vt_host_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res) {
+  return host_transcode(in, n, out, n, res,
+                        [](const uint8_t* i, uint64_t k, uint16_t* o, vt_result* r, cudaStream_t s) {
+                          return run_utf8(i, k, o, r, s, true);
+                        });
+}
+
+int vt_host_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, vt_result* res) {
+  return host_transcode(in, n, out, 3 * n + 16, res,
+                        [](const uint16_t* i, uint64_t k, uint8_t* o, vt_result* r, cudaStream_t s) {
+                          return run_utf16(i, k, o, r, s, true);
+                        });
+}
+
+int vt_host_validate_utf8(const uint8_t* in, uint64_t n, int64_t* first_err) {
+  if (!first_err) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint8_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf8(i, k, nullptr, d, s, false);
+  }));
+  *first_err = r.error_at;
+  return 0;
+}
+
+int vt_host_validate_utf16(const uint16_t* in, uint64_t n, int64_t* first_err) {
+  if (!first_err) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf16(i, k, nullptr, d, s, false);
+  }));
+  *first_err = r.error_at;
+  return 0;
+}
+
+int vt_host_count_utf8(const uint8_t* in, uint64_t n, int64_t* count) {
+  if (!count) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint8_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf8(i, k, nullptr, d, s, false);
+  }));
+  *count = r.error_at < 0 ? (int64_t)r.written : -1;
+  return 0;
+}
+
+int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count) {
+  if (!count) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf16(i, k, nullptr, d, s, false);
+  }));
+  *count = r.error_at < 0 ? (int64_t)r.written : -1;
+  return 0;
+}
+
+int vt_validate_utf8_batch(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           int64_t* d_first_err, vt_stream stream) {
+  int dev;
+  VT_TRY(current_device(dev));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_validate_utf8_batch(d_data, d_offsets, count, d_first_err,
+                                        (cudaStream_t)stream);
+}
+
+int vt_exhaustive_short_verdicts(uint8_t* d_verdicts, vt_stream stream) {
+  int dev;
+  VT_TRY(current_device(dev));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_exhaustive_short(d_verdicts, (cudaStream_t)stream);
+}
+
+// ---- sharder -------------------------------------------------------------------
+
+uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut) {
+  // move the cut back to the last non-continuation byte
+  // within 3 bytes; if there is none, no valid character spans the cut.
+  if (cut == 0 || cut >= n) return cut;
+  for (uint64_t k = 0; k <= 3 && k <= cut; k++)
+    if ((in[cut - k] & 0xC0) != 0x80) return cut - k;
+  return cut;
+}
+
+uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut) {
+  // fact E: never separate a high surrogate from the low one that follows it
+  if (cut == 0 || cut >= n) return cut;
+  if ((in[cut] & 0xFC00) == 0xDC00 && (in[cut - 1] & 0xFC00) == 0xD800) return cut - 1;
+  return cut;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <class In, class Out, class Split, class One>
+int sharded(const In* in, uint64_t n, Out* out, int ndev, uint64_t mult, vt_result* res,
+            Split split, One one) {
+  if (!res || (n && (!in || !out))) return VT_E_ARG;
+  int avail = 0;
+  if (cudaGetDeviceCount(&avail) != cudaSuccess || avail == 0) {
+    cudaGetLastError();
+    return VT_E_NODEVICE;
+  }
+  // ndev shards; shard k runs on device k % avail (more shards than devices
+  // share a device, each on its own host thread and stream)
+  if (ndev <= 0) ndev = avail;
+  std::vector<uint64_t> st(ndev + 1, 0);
+  for (int k = 1; k < ndev; k++) st[k] = std::max(st[k - 1], split(in, n, n / ndev * k));
+  st[ndev] = n;
+  std::vector<vt_result> rs(ndev);
+  std::vector<int> rcs(ndev, 0);
+  std::vector<std::thread> ts;
+  for (int k = 0; k < ndev; k++) {
+    ts.emplace_back([&, k] {
+      rcs[k] = (int)cudaSetDevice(k % avail);
+      if (rcs[k]) return;
+      // shard k's output fits in [mult*st[k], mult*st[k+1]) of the caller's buffer
+      rcs[k] = one(in + st[k], st[k + 1] - st[k], out + mult * st[k], &rs[k]);
+    });
+  }
+  for (auto& t : ts) t.join();
+  for (int k = 0; k < ndev; k++)
+    if (rcs[k]) return rcs[k];
+  // combine: exclusive scan of written, first failing shard decides
+  uint64_t written = 0;
+  res->error_at = -1;
+  res->consumed = n;
+  for (int k = 0; k < ndev; k++) {
+    if (written != mult * st[k] && rs[k].written)
+      std::memmove(out + written, out + mult * st[k], rs[k].written * sizeof(Out));
+    written += rs[k].written;
+    if (rs[k].error_at >= 0) {
+      res->error_at = (int64_t)st[k] + rs[k].error_at;
+      res->consumed = (uint64_t)res->error_at;
+      break;
+    }
+  }
+  res->written = written;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vt_sharded_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, int ndev,
+                             vt_result* res) {
+  return sharded(in, n, out, ndev, 1, res, vt_split_point_utf8, vt_host_utf8_to_utf16);
+}
+
+int vt_sharded_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, int ndev,
+                             vt_result* res) {
+  return sharded(in, n, out, ndev, 3, res, vt_split_point_utf16, vt_host_utf16_to_utf8);
+}
+
+int vt_gen_sizes(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks, uint64_t* d_sizes,
+                 vt_stream stream) {
+  if (cfg < 1 || cfg > 5) return VT_E_ARG;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_gen_sizes(cfg, seed, chunk0, nchunks, d_sizes, (cudaStream_t)stream);
+}
+
+int vt_gen_write(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks,
+                 const uint64_t* d_offsets, uint64_t limit, void* d_out, uint64_t* d_end,
+                 vt_stream stream) {
+  if (cfg < 1 || cfg > 5) return VT_E_ARG;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_gen_write(cfg, seed, chunk0, nchunks, d_offsets, limit, d_out, d_end,
+                              (cudaStream_t)stream);
+}
+
+const char* vt_status_string(int status) {
+  if (status == 0) return "ok";
+  if (status == VT_E_NODEVICE) return "no CUDA device visible (libvtrans_gpu has no CPU fallback)";
+  if (status == VT_E_ARG) return "invalid argument";
+  if (status == VT_E_ARCH) return "device is not sm_100 (kernels are built for sm_100a only)";
+  return cudaGetErrorString((cudaError_t)status);
+}
+
+int vt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+uint64_t vt_launch_count(void) { return g_launches.load(); }
+
+const char* vt_build_info(void) {
+  return "libvtrans_gpu sm_100a (nvcc " VT_STR(__CUDACC_VER_MAJOR__) "." VT_STR(
+      __CUDACC_VER_MINOR__) ")";
+}
+
+}  // extern "C"

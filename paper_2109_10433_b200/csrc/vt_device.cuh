@@ -1,0 +1,202 @@
+// vt_device.cuh -- shared sm_100a device machinery for the transcoding kernels.
+//
+//  * tile scheduling: persistent CTAs pull tile ids from an atomic counter, so
+//    every tile's predecessors are owned by CTAs that are already running
+//    (the forward-progress condition of the decoupled look-back);
+//  * the single-pass decoupled look-back scan over per-tile output counts
+//    (epoch-tagged 64-bit status words: no per-call memset of the status array);
+//  * first-error resolution across tiles (atomicMin on the input position;
+//    tiles behind a known error stop early, like the reference's early exit at
+//    proj/src/utf8_to_utf16.cpp:121,144 and proj/src/validation.cpp:38);
+//  * the "last CTA finalises" epilogue that writes the TranscodeResult and
+//    re-arms the control block for the next call on the same scratch;
+//  * an aligned 16-byte copy-out from the shared-memory staging buffer to an
+//    arbitrarily aligned global destination.
+#pragma once
+
+#include <cstdint>
+#include <cuda/atomic>
+
+#include "../../include/vtrans_gpu.h"
+
+namespace vt {
+
+constexpr unsigned long long kNoError = ~0ull;
+
+// PRMT in its default mode: selector nibble bit 3 replicates the sign bit of the
+// selected byte (the 16-entry lookup trick in k_utf8.cu depends on it).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Per-call control block.  Zeroed once at allocation; the finalising CTA of
+// every launch re-arms it, so consecutive calls on one stream need no memset.
+struct Ctl {
+  unsigned int tile_counter;
+  unsigned int done;
+  unsigned long long err;    // smallest failing input index seen, kNoError if none
+  unsigned long long count;  // validate/count kernels: code points in the valid prefix
+  unsigned long long pad[5];
+};
+
+// ---- status words -----------------------------------------------------------
+// [63:62] flag (1 = aggregate, 2 = inclusive prefix), [61:48] epoch, [47:0] value
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 48) - 1;
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned long long flag, unsigned epoch,
+                                                          unsigned long long v) {
+  return flag | ((unsigned long long)(epoch & 0x3FFF) << 48) | (v & kValMask);
+}
+
+__device__ __forceinline__ void store_status(unsigned long long* p, unsigned long long s) {
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
+  a.store(s, cuda::memory_order_relaxed);
+}
+
+__device__ __forceinline__ unsigned long long load_status(unsigned long long* p) {
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
+  return a.load(cuda::memory_order_relaxed);
+}
+
+__device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p) {
+  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
+  return a.load(cuda::memory_order_relaxed);
+}
+
+// Warp-cooperative decoupled look-back for tile `tile` (> 0), executed by one
+// full warp.  Returns the exclusive prefix, or ~0ull when the tile became
+// irrelevant (a tile before it reported an error, so its output is never read).
+// Looks at 32 predecessors per step: lane i inspects tile (base - i).
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* status, unsigned epoch,
+                                                      unsigned tile, const Ctl* ctl,
+                                                      unsigned long long tile_bytes,
+                                                      unsigned long long head) {
+  const unsigned lane = threadIdx.x & 31;
+  unsigned long long excl = 0;
+  long long base = (long long)tile - 1;
+  unsigned spins = 0;
+  while (true) {
+    const long long idx = base - (long long)lane;
+    unsigned long long s = 0;
+    bool ready = true;
+    if (idx >= 0) {
+      s = load_status(&status[idx]);
+      ready = ((s >> 62) != 0) && (((s >> 48) & 0x3FFF) == (epoch & 0x3FFF));
+    }
+    // lanes past tile 0 behave like an inclusive prefix of 0
+    const bool is_pre = idx < 0 || (ready && (s >> 62) == 2);
+    const unsigned ready_mask = __ballot_sync(0xffffffffu, ready || idx < 0);
+    const unsigned pre_mask = __ballot_sync(0xffffffffu, is_pre);
+    // the contiguous run of ready lanes starting at lane 0
+    const unsigned run = ready_mask == 0xffffffffu ? 32u : (unsigned)__ffs(~ready_mask) - 1u;
+    const unsigned pre_in_run = pre_mask & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
+    if (pre_in_run) {
+      const unsigned stop = (unsigned)__ffs(pre_in_run) - 1u;  // nearest inclusive prefix
+      unsigned long long v = (lane <= stop && idx >= 0) ? (s & kValMask) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      return excl + v;
+    }
+    if (run > 0) {
+      unsigned long long v = (lane < run) ? (s & kValMask) : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      excl += v;
+      base -= (long long)run;
+      continue;
+    }
+    // nothing ready yet: give up if an earlier tile failed (our output is dead)
+    const unsigned long long e = load_relaxed(const_cast<unsigned long long*>(&ctl->err));
+    if (e != kNoError && (e + head) / tile_bytes < tile) return ~0ull;
+    if (++spins > 8) __nanosleep(32);
+  }
+}
+
+// Copies `len` bytes from shared memory `src` (16-byte aligned) to global `dst`
+// (any alignment) with aligned 16-byte stores in the body.  The whole CTA
+// participates.  `src` must have >= 16 readable bytes before and after.
+__device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
+                                         unsigned len) {
+  if (len == 0) return;
+  const uintptr_t d0 = (uintptr_t)dst;
+  const unsigned mis = (unsigned)(d0 & 15);  // dst chunk c covers src bytes [16c - mis, 16c - mis + 16)
+  const unsigned nchunks = (mis + len + 15) >> 4;
+  uint8_t* dbase = dst - mis;
+  const unsigned ws = (16 - mis) & 15;  // source offset of chunk c is 16c - mis = 16(c-1) + ws
+  for (unsigned c = threadIdx.x; c < nchunks; c += blockDim.x) {
+    // gather 16 source bytes starting at src + 16c - mis
+    const int so = (int)(16 * c) - (int)mis;
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src + ((so >> 2) << 2) - 0);
+    uint32_t w[5];
+    // so may be negative for c == 0 (the first chunk); src has >= 16 bytes of slack before
+#pragma unroll
+    for (int i = 0; i < 5; i++) w[i] = s32[i];
+    const unsigned bs = (unsigned)(so & 3) * 8;
+    uint4 v;
+    v.x = __funnelshift_r(w[0], w[1], bs);
+    v.y = __funnelshift_r(w[1], w[2], bs);
+    v.z = __funnelshift_r(w[2], w[3], bs);
+    v.w = __funnelshift_r(w[3], w[4], bs);
+    uint8_t* d = dbase + 16 * c;
+    const bool full = (c > 0 || mis == 0) && (16 * c + 16 <= mis + len);
+    if (full) {
+      *reinterpret_cast<uint4*>(d) = v;
+    } else {
+      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int b = 0; b < 16; b++) {
+        const unsigned pos = 16 * c + b;  // relative to dbase
+        if (pos >= mis && pos < mis + len) d[b] = (uint8_t)(vv[b >> 2] >> ((b & 3) * 8));
+      }
+    }
+  }
+  (void)ws;
+}
+
+// Block-wide exclusive scan of one unsigned per thread (THREADS threads).
+template <int THREADS>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_sums,
+                                                    unsigned& total) {
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned t = lane < THREADS / 32 ? warp_sums[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < THREADS / 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= (unsigned)o) t += y;
+    }
+    if (lane < THREADS / 32) warp_sums[lane] = t;  // inclusive warp prefixes
+  }
+  __syncthreads();
+  total = warp_sums[THREADS / 32 - 1];
+  const unsigned wbase = wid ? warp_sums[wid - 1] : 0u;
+  return wbase + x - v;
+}
+
+template <int THREADS>
+__device__ __forceinline__ unsigned block_min(unsigned v, unsigned* scratch) {
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  unsigned r = scratch[0];
+#pragma unroll
+  for (int i = 1; i < THREADS / 32; i++) r = min(r, scratch[i]);
+  __syncthreads();
+  return r;
+}
+
+}  // namespace vt

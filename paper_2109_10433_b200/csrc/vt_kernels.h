@@ -1,0 +1,63 @@
+// vt_kernels.h -- host-visible launch interface of the sm_100a kernels
+// (internal to libvtrans_gpu.so; the public boundary is include/vtrans_gpu.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/vtrans_gpu.h"
+
+namespace vt {
+
+struct Ctl;
+
+// UTF-8 side: `base` is the input rounded down to 16 bytes, `head` the offset
+// of the first input byte from it.  Tiles cover virtual bytes [0, head + n).
+struct U8Args {
+  const uint8_t* base;
+  unsigned long long head;
+  unsigned long long n;
+  unsigned ntiles;
+  unsigned epoch;
+  uint16_t* out;
+  unsigned long long* status;
+  Ctl* ctl;
+  vt_result* res;
+};
+
+// UTF-16 side: same conventions in units (`head` in units, 0..7).
+struct U16Args {
+  const uint16_t* base;
+  unsigned long long head;
+  unsigned long long n;
+  unsigned ntiles;
+  unsigned epoch;
+  uint8_t* out;
+  unsigned long long* status;
+  Ctl* ctl;
+  vt_result* res;
+};
+
+int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s);
+int occupancy_utf8(bool transcode);
+unsigned tiles_utf8(unsigned long long head, unsigned long long n);
+
+int launch_utf16(const U16Args& a, bool transcode, int grid, cudaStream_t s);
+int occupancy_utf16(bool transcode);
+unsigned tiles_utf16(unsigned long long head, unsigned long long n);
+
+// Batched validation of many short strings (one warp per string).
+int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                               int64_t* first_err, cudaStream_t s);
+// Every 1/2/3-byte input (acceptance C3 order), verdict per input.
+int launch_exhaustive_short(uint8_t* verdicts, cudaStream_t s);
+
+// Synthetic workload generators (bench.py / tests): see k_datagen.cu.
+int launch_gen_sizes(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks, uint64_t* sizes,
+                     cudaStream_t s);
+int launch_gen_write(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks,
+                     const uint64_t* offsets, uint64_t limit, void* out, uint64_t* end_pos,
+                     cudaStream_t s);
+
+}  // namespace vt

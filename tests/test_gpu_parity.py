@@ -1,0 +1,376 @@
+"""GPU parity: the sm_100a kernels against the oracle, bit for bit.
+
+Every check compares output units/bytes, consumed, written and error_at (the
+full TranscodeResult, proj/include/vtrans/codec_core.hpp:14-21) with the C
+restatement of the reference's scalar codec (oracle/, pinned in
+test_oracle.py) or with the committed golden vectors.  Calls go through the C
+ABI (host-pointer entry points = the drop-in boundary; device-pointer entry
+points for alignment sweeps and BASELINE-size inputs).
+"""
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2109_10433_b200 as vt
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _u16(hexstr):
+    return np.frombuffer(bytes.fromhex(hexstr), dtype="<u2").astype(np.uint16)
+
+
+def _same(r, want):
+    return (r.consumed, r.written, r.error_at) == (want.consumed, want.written, want.error_at)
+
+
+# ---- golden vectors (reference KATs + seeded differential cases) ---------------
+
+def test_golden_utf8(golden):
+    for c in golden["u8"]:
+        data = bytes.fromhex(c["in"])
+        out, r = vt.utf8_to_utf16(data)
+        assert (r.consumed, r.written, r.error_at) == (c["consumed"], c["written"], c["error_at"]), c["src"]
+        if "out" in c:
+            assert [int(x) for x in out] == c["out"], c["src"]
+        else:
+            assert hashlib.sha1(out.astype("<u2").tobytes()).hexdigest() == c["out_sha1"], c["src"]
+        assert vt.validate_utf8(data) == c["valid"], c["src"]
+        assert vt.count_utf8(data) == c["count"], c["src"]
+
+
+def test_golden_utf16(golden):
+    for c in golden["u16"]:
+        units = _u16(c["in"])
+        out, r = vt.utf16_to_utf8(units)
+        assert (r.consumed, r.written, r.error_at) == (c["consumed"], c["written"], c["error_at"]), c["src"]
+        if "out" in c:
+            assert bytes(out).hex() == c["out"], c["src"]
+        else:
+            assert hashlib.sha1(out.tobytes()).hexdigest() == c["out_sha1"], c["src"]
+        assert vt.validate_utf16(units) == c["validate16"], c["src"]
+        assert vt.count_utf16(units) == c["count"], c["src"]
+
+
+def test_exhaustive_short_inputs(golden, torch):
+    """acceptance.cpp:138-167 (C3): every 1/2/3-byte input, on the GPU."""
+    v = vt.exhaustive_short_verdicts().cpu().numpy()
+    e = golden["misc"]["exhaustive_short"]
+    assert int(v.sum()) == e["valid"]
+    assert hashlib.sha256(v.tobytes()).hexdigest() == e["sha256"]
+    # and the same verdicts through the tiled kernel for a sample of them
+    rng = np.random.default_rng(3)
+    for k in rng.integers(0, len(v), 3000):
+        k = int(k)
+        ln, x = (1, k) if k < 256 else (2, k - 256) if k < 65792 else (3, k - 65792)
+        b = bytes((x >> (8 * (ln - 1 - i))) & 0xFF for i in range(ln))
+        assert vt.validate_utf8(b) == bool(v[k])
+
+
+# ---- alignment / length sweeps (acceptance C5) ----------------------------------
+
+def test_lengths_and_offsets_utf8(oracle, torch):
+    """acceptance.cpp:208-229: lengths 0..256 x start offsets 0..15, plus
+    misaligned output pointers, through the device-pointer ABI."""
+    pat = bytearray()
+    while len(pat) < 300:
+        pat += bytes([0x61, 0xC2, 0xA3, 0xE9, 0x8F, 0xA1, 0xF0, 0x90, 0x8D, 0x88, 0x62, 0x63, 0xD9,
+                      0x84, 0xE4, 0xB8, 0xAD])
+    buf = torch.zeros(512, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    for ln in range(0, 257):
+        want_out, want = oracle.utf8_to_utf16(bytes(pat[:ln]))
+        for off in range(16):
+            arr = np.zeros(512, dtype=np.uint8)
+            arr[off:off + ln] = np.frombuffer(bytes(pat[:ln]), dtype=np.uint8)
+            buf.copy_(torch.from_numpy(arr))
+            ooff = 2 * ((ln + off) % 8)
+            out.fill_(0xEE)
+            # UTF-16 output at a 2-byte (not 16-byte) aligned address
+            o16 = out[ooff:].view(torch.int16)
+            r = vt.utf8_to_utf16_device(buf, ln, o16, offset=off)
+            assert _same(r, want), (ln, off)
+            got = out[ooff:ooff + 2 * r.written].cpu().numpy().view("<u2")
+            assert np.array_equal(got, want_out), (ln, off)
+            # nothing before the output start was touched
+            assert (out[:ooff].cpu().numpy() == 0xEE).all()
+
+
+def test_lengths_and_offsets_utf16(oracle, torch):
+    """acceptance.cpp:231-249: UTF-16 pattern with pairs broken by the cut."""
+    units = np.array([[0x0041, 0x93E1, 0xD852, 0xDF62, 0x00E9][i % 5] for i in range(300)], dtype=np.uint16)
+    buf = torch.zeros(600, dtype=torch.int16, device="cuda")
+    out = torch.zeros(2048, dtype=torch.uint8, device="cuda")
+    for ln in range(0, 257):
+        want_out, want = oracle.utf16_to_utf8(units[:ln])
+        for off in range(8):
+            arr = np.zeros(600, dtype=np.uint16)
+            arr[off:off + ln] = units[:ln]
+            buf.copy_(torch.from_numpy(arr.view(np.int16)))
+            ooff = (ln * 7 + off) % 16
+            out.fill_(0xEE)
+            r = vt.utf16_to_utf8_device(buf, ln, out[ooff:], offset=2 * off)
+            assert _same(r, want), (ln, off)
+            assert np.array_equal(out[ooff:ooff + r.written].cpu().numpy(), want_out), (ln, off)
+            assert (out[:ooff].cpu().numpy() == 0xEE).all()
+
+
+# ---- tile / row / thread seams ------------------------------------------------------
+
+SEAMS = [0, 1, 2, 3, 15, 16, 17, 4093, 4094, 4095, 4096, 4097, 8189, 8190, 8191, 8192, 8193,
+         8194, 16383, 16384, 16385, 24575, 24576]
+
+
+def test_multibyte_across_seams(oracle):
+    """A character of every length straddling every tile/row/thread seam, at
+    several start alignments; truncations and broken continuations there."""
+    seqs = [bytes([0xC2, 0xA3]), bytes([0xE9, 0x8F, 0xA1]), bytes([0xF0, 0x9F, 0x98, 0x80])]
+    for pre in (0, 5, 11):
+        for seam in SEAMS[4:]:
+            for s in seqs:
+                for split in range(1, len(s)):
+                    base = bytearray(b"x" * (pre + seam - split)) + s + b"y" * 70
+                    for data in (bytes(base), bytes(base[: pre + seam]),
+                                 bytes(base[: pre + seam] + b"A" + base[pre + seam + 1:])):
+                        want_out, want = oracle.utf8_to_utf16(data[pre:])
+                        out, r = vt.utf8_to_utf16(data[pre:])
+                        assert _same(r, want), (pre, seam, s.hex(), split)
+                        assert np.array_equal(out, want_out)
+
+
+def test_errors_at_seams(oracle):
+    """proj/tests/test_utf8_to_utf16.cpp:159-171 generalised to GPU seams: one
+    bad byte of each class at every seam, in ASCII and in CJK context."""
+    bad = [b"\xff", b"\x80", b"\xc0\xaf", b"\xe0\x80\x80", b"\xed\xa0\x80", b"\xf4\x90\x80\x80", b"\xe9\x8f"]
+    for ctx in (b"a", "中".encode()):
+        base = ctx * (40000 // len(ctx))
+        for seam in SEAMS:
+            for b in bad:
+                p = seam - seam % len(ctx)
+                data = base[:p] + b + base[p:]
+                want_out, want = oracle.utf8_to_utf16(data)
+                out, r = vt.utf8_to_utf16(data)
+                assert _same(r, want), (ctx, seam, b.hex())
+                assert np.array_equal(out, want_out)
+
+
+def test_utf16_pairs_across_seams(oracle):
+    for seam in [1, 7, 8, 9, 2047, 2048, 2049, 4095, 4096, 4097, 8191, 8192]:
+        for mode in range(3):
+            u = np.full(12000, 0x93E1, dtype=np.uint16)
+            u[seam - 1], u[seam] = 0xD83D, 0xDE00
+            if mode == 1:
+                u[seam] = 0x0041  # unpaired high
+            if mode == 2:
+                u[seam - 1] = 0x0041  # lone low
+            want_out, want = oracle.utf16_to_utf8(u)
+            out, r = vt.utf16_to_utf8(u)
+            assert _same(r, want) and np.array_equal(out, want_out), (seam, mode)
+            assert vt.validate_utf16(u) == oracle.validate_utf16(u)
+
+
+# ---- differential fuzz (cf. proj/src/harness.cpp:388-436) ---------------------------
+
+def _gen_text(rng, n, mix):
+    cls = rng.choice(4, size=n, p=np.asarray(mix) / sum(mix))
+    lo = np.array([0, 0x80, 0x800, 0x10000])[cls]
+    hi = np.array([0x80, 0x800, 0x10000, 0x110000])[cls]
+    cps = lo + (rng.random(n) * (hi - lo)).astype(np.int64)
+    cps = np.where((cps >= 0xD800) & (cps <= 0xDFFF), cps - 0x800, cps)
+    return "".join(map(chr, cps.tolist()))
+
+
+def test_random_differential(oracle):
+    rng = np.random.default_rng(20260823)
+    mixes = [(100, 0, 0, 0), (22, 78, 0, 0), (1, 0, 99, 0), (0, 0, 0, 100), (25, 25, 25, 25), (50, 0, 50, 0)]
+    for it in range(1500):
+        kind = it % 3
+        n = int(rng.choice([int(rng.integers(0, 300)), int(rng.integers(0, 40000))]))
+        if kind == 0:
+            data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        else:
+            data = bytearray(_gen_text(rng, max(1, n // 2), mixes[it % 6]).encode()[:n])
+            if kind == 2 and data:
+                for _ in range(int(rng.integers(1, 4))):
+                    data[int(rng.integers(0, len(data)))] ^= 1 << int(rng.integers(0, 8))
+            data = bytes(data)
+        want_out, want = oracle.utf8_to_utf16(data)
+        out, r = vt.utf8_to_utf16(data)
+        assert _same(r, want), (it, n)
+        assert np.array_equal(out, want_out), it
+        assert vt.first_error_utf8(data) == want.error_at
+        if want.error_at is None:
+            assert vt.count_utf8(data) == oracle.count_utf8(data)
+            back, rb = vt.utf16_to_utf8(out)  # round trip (harness.cpp:366-372)
+            assert rb.error_at is None and back.tobytes() == data
+        u = rng.integers(0, 65536, n // 2, dtype=np.uint16) if kind == 0 else \
+            np.frombuffer(data.decode("utf-8", "replace").encode("utf-16-le"), dtype=np.uint16).copy()
+        if kind == 2 and len(u):
+            u[int(rng.integers(0, len(u)))] ^= 1 << int(rng.integers(0, 16))
+        want8, w16 = oracle.utf16_to_utf8(u)
+        out8, r16 = vt.utf16_to_utf8(u)
+        assert _same(r16, w16) and np.array_equal(out8, want8), it
+        assert vt.validate_utf16(u) == w16.error_at
+
+
+def test_batch_validation(oracle, torch):
+    rng = np.random.default_rng(77)
+    strings = []
+    for i in range(20000):
+        n = int(rng.integers(0, 257))
+        if i % 2:
+            strings.append(rng.integers(0, 256, n, dtype=np.uint8).tobytes())
+        else:
+            b = bytearray(_gen_text(rng, max(1, n // 2), (25, 25, 25, 25)).encode()[:n])
+            if b and i % 4 == 0:
+                b[int(rng.integers(0, len(b)))] ^= 1 << int(rng.integers(0, 8))
+            strings.append(bytes(b))
+    offs = np.zeros(len(strings) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(s) for s in strings])
+    data = torch.frombuffer(bytearray(b"".join(strings)) or bytearray(1), dtype=torch.uint8).cuda()
+    d_offs = torch.from_numpy(offs).cuda()
+    d_err = torch.empty(len(strings), dtype=torch.int64, device="cuda")
+    vt.validate_utf8_batch(data, d_offs, len(strings), d_err)
+    got = d_err.cpu().numpy()
+    for i, s in enumerate(strings):
+        e = oracle.validate_utf8(s)
+        assert got[i] == (-1 if e is None else e), i
+
+
+# ---- BASELINE.json configurations at full size ---------------------------------------
+
+def _threads():
+    return max(2, min(64, os.cpu_count() or 2))
+
+
+@pytest.mark.parametrize("cfg,size", [(1, 16 << 20), (2, 1 << 30), (4, 1 << 30)])
+def test_config_utf8_full_size(cfg, size, oracle, torch):
+    d_in, n, first_bad = vt.generate(cfg, size)
+    assert size - 4 <= n <= size
+    d_out = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+    r = vt.utf8_to_utf16_device(d_in, n, d_out)
+    host = d_in[:n].cpu().numpy()
+    want_out, want = oracle.utf8_to_utf16(host, threads=_threads())
+    assert _same(r, want)
+    got = d_out[: r.written].cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, want_out)
+    if cfg == 4:
+        assert want.error_at == first_bad  # the generator's first injection
+        v = vt.validate_utf8_device(d_in, n)
+        assert v.error_at == want.error_at
+    else:
+        assert want.error_at is None
+        v = vt.validate_utf8_device(d_in, n)
+        assert v.error_at is None and v.written == oracle.count_utf8(host)
+
+
+def test_config3_utf16_full_size(oracle, torch):
+    d_in, n, _ = vt.generate(3, 1 << 29)  # 1 GiB of UTF-16LE = 2^29 units
+    d_out = torch.empty(3 * n + 16, dtype=torch.uint8, device="cuda")
+    r = vt.utf16_to_utf8_device(d_in, n, d_out)
+    host = d_in[:n].cpu().numpy().view(np.uint16)
+    want_out, want = oracle.utf16_to_utf8(host, threads=_threads())
+    assert _same(r, want) and want.error_at is None
+    assert np.array_equal(d_out[: r.written].cpu().numpy(), want_out)
+    v = vt.validate_utf16_device(d_in, n)
+    assert v.error_at is None and v.written == oracle.count_utf16(host)
+
+
+def test_config5_round_trip_4gib(torch):
+    """cfg 5 on one GPU: 4 GiB of UTF-8 -> UTF-16 -> UTF-8 must reproduce the
+    input byte for byte (size-independent property at the full shard size)."""
+    d_in, n, _ = vt.generate(5, 4 << 30)
+    d16 = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+    r1 = vt.utf8_to_utf16_device(d_in, n, d16)
+    assert r1.error_at is None and r1.consumed == n
+    d8 = torch.empty(3 * r1.written + 16, dtype=torch.uint8, device="cuda")
+    r2 = vt.utf16_to_utf8_device(d16, r1.written, d8)
+    assert r2.error_at is None and r2.written == n
+    assert torch.equal(d8[:n], d_in[:n])
+    # code points agree between the two encodings
+    c8 = vt.validate_utf8_device(d_in, n).written
+    c16 = vt.validate_utf16_device(d16, r1.written).written
+    assert c8 == c16
+
+
+def test_sharder_single_process(oracle):
+    """In-process sharder: 5 shards over the visible GPU(s), combine exact."""
+    rng = np.random.default_rng(9)
+    text = _gen_text(rng, 300000, (60, 15, 15, 10)).encode()
+    for k in (1, 3, 5):
+        for err in (None, len(text) // 2 + 1, len(text) - 2):
+            data = bytearray(text)
+            if err is not None:
+                data[err] = 0xFF
+            data = bytes(data)
+            want_out, want = oracle.utf8_to_utf16(data)
+            out, r = vt.sharded_utf8_to_utf16(data, k)
+            assert _same(r, want) and np.array_equal(out, want_out), (k, err)
+            u = np.frombuffer(text.decode().encode("utf-16-le"), dtype=np.uint16).copy()
+            if err is not None:
+                u[err // 2] = 0xDC00
+            w8, w16 = oracle.utf16_to_utf8(u)
+            o8, r16 = vt.sharded_utf16_to_utf8(u, k)
+            assert _same(r16, w16) and np.array_equal(o8, w8), (k, err)
+
+
+def test_drop_in_cxx_program(tmp_path):
+    """A C++ program written against the reference API (vtrans/*.hpp) links
+    against libvtrans_gpu.so unchanged and gets the reference's answers."""
+    src = tmp_path / "dropin.cpp"
+    src.write_text(r'''
+#include "vtrans/utf8_to_utf16.hpp"
+#include "vtrans/utf16_to_utf8.hpp"
+#include "vtrans/validation.hpp"
+#include <cstdio>
+int main() {
+  std::vector<uint8_t> in{0x24, 0xC2, 0xA3, 0xE9, 0x8F, 0xA1, 0xF0, 0x90, 0x8D, 0x88};
+  vtrans::TranscodeResult r;
+  auto out = vtrans::utf8_to_utf16(in, true, r);
+  bool ok = r.ok() && out == std::vector<uint16_t>{0x0024, 0x00A3, 0x93E1, 0xD800, 0xDF48};
+  std::vector<uint8_t> bad{0x41, 0xC2, 0xA3, 0xFF, 0x42};
+  auto o2 = vtrans::utf8_to_utf16(bad, true, r);
+  ok = ok && r.error_at && *r.error_at == 3 && r.consumed == 3 && r.written == 2;
+  std::vector<uint16_t> u{0x0041, 0xD800, 0x0042};
+  auto o3 = vtrans::utf16_to_utf8(u, r);
+  ok = ok && r.error_at == 1 && r.written == 1 && !vtrans::validate_utf8(bad);
+  ok = ok && vtrans::validate_utf16(u) == std::optional<std::size_t>(1);
+  std::printf("%s\n", ok ? "DROPIN OK" : "DROPIN FAIL");
+  return ok ? 0 : 1;
+}
+''')
+    exe = tmp_path / "dropin"
+    libdir = os.path.dirname(vt.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-O1", str(src), "-I", os.path.join(ROOT, "include"), "-L", libdir,
+                    "-lvtrans_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0 and "DROPIN OK" in p.stdout, p.stdout + p.stderr
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_gpu")
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.path.exists(ACC), reason="oracle/_ref/acceptance_gpu not built")
+def test_reference_acceptance_harness_on_gpu():
+    """The reference's own acceptance.cpp (built out of tree, oracle/Makefile)
+    linked against OUR library: criteria 1-7 and 10 must pass; C8 (CPU SIMD
+    speed ratios) and C9 (CPU branch counters) are CPU-mechanism criteria
+     and are reported, not required."""
+    p = subprocess.run([ACC], capture_output=True, text=True, timeout=1500)
+    print(p.stdout)
+    lines = {int(l.split(":")[0].split()[1]): l for l in p.stdout.splitlines() if l.startswith("criterion")}
+    for c in (1, 2, 3, 4, 5, 6, 7, 10):
+        assert "PASS" in lines[c], lines.get(c)
