@@ -182,6 +182,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
   __syncthreads();
   total = warp_sums[THREADS / 32 - 1];
   const unsigned wbase = wid ? warp_sums[wid - 1] : 0u;
+  __syncthreads();  // warp_sums is reused by the next scan
   return wbase + x - v;
 }
 
