@@ -3,65 +3,40 @@
 //
 // Replaces the reference's 64-byte block driver (proj/src/utf8_to_utf16.cpp:
 // 88-226) and the nibble-table checker (proj/include/vtrans/utf8_checker.hpp:
-// 28-137).  One persistent kernel does, per 8 KiB tile:
-//   1. coalesced 16-byte loads of the tile plus a 16-byte halo on each side
-//      into shared memory (zero-filled outside the input, which makes the
-//      start and the end of the input behave like the reference's zero-padded
-//      final block, proj/src/validation.cpp:41-47);
-//   2. per-thread SWAR classification of 16 bytes: continuation / 2-, 3-,
-//      4-byte lead bit planes, the lead/continuation structure check and the
-//      value-range check of the special leads (C0 C1 E0 ED F0 F4..FF);
-//   3. on any flag, the exact per-byte first-error rule (SURVEY.md 8(a) fact
-//      A) over the thread's bytes -- the scalar decoder's error_at
-//      (proj/src/codec_core.cpp:85-104) without a sequential re-scan;
-//   4. output length per thread (one unit per character, two for 4-byte
-//      characters), block scan, decoupled look-back for the tile offset;
-//   5. decode into a shared-memory staging buffer and aligned 16-byte stores.
+// 28-137).  One persistent kernel; per 16 KiB tile, each thread owns 64
+// contiguous bytes (16 words):
+//   A. SWAR classification, 4 bytes per 32-bit op: continuation / >=C0 /
+//      >=E0 / >=F0 bit planes, the lead/continuation structure check (a byte
+//      must be a continuation iff a lead 1..3 bytes back requires it), and a
+//      cheap filter for the only leads whose value range needs checking
+//      (C0 C1, E0 ED EE EF; F0..FF go to the 4-byte path).  Counting is
+//      SWAR too: units = characters + 4-byte characters.
+//   B. any flag -> the exact first-error rule of SURVEY.md 8(a) fact A over
+//      the thread's bytes (the scalar decoder's error_at, proj/src/
+//      codec_core.cpp:85-104, without a sequential re-scan);
+//   C. block scan + decoupled look-back for the output offset;
+//   D. branch-free SWAR decode of BMP characters (lead-attributed byte planes:
+//      low and high byte of each character's UTF-16 unit), predicated 16-bit
+//      stores into a shared-memory staging buffer; threads with 4-byte or
+//      range-checked leads decode per character instead;
+//   E. aligned 16-byte stores of the staged tile to the (arbitrarily aligned)
+//      output.
+// Tiles at the ends of the input (partial, or whose halo leaves the input)
+// and tiles containing an error take a simple masked per-character path.
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
 namespace vt {
 
-constexpr int U8_THREADS = 256;
-constexpr int U8_ROWS = 2;
-constexpr int U8_ROW = U8_THREADS * 16;   // bytes per row
-constexpr int U8_TILE = U8_ROW * U8_ROWS;  // bytes per tile
+constexpr int K8_THREADS = 256;
+constexpr int K8_WPT = 16;                      // words per thread
+constexpr int K8_BPT = 4 * K8_WPT;              // bytes per thread
+constexpr int K8_TILE = K8_THREADS * K8_BPT;    // bytes per tile
 constexpr unsigned kNone = 0xFFFFFFFFu;
-
-// ---- byte-plane masks (bit 7 of each byte lane) ----------------------------
-__device__ __forceinline__ uint32_t hi_bits(uint32_t x) { return x & 0x80808080u; }
-__device__ __forceinline__ uint32_t m_cont(uint32_t x) { return x & ~(x << 1) & 0x80808080u; }
-__device__ __forceinline__ uint32_t m_ge_c0(uint32_t x) { return x & (x << 1) & 0x80808080u; }
-__device__ __forceinline__ uint32_t m_ge_e0(uint32_t x) { return m_ge_c0(x) & (x << 2); }
-__device__ __forceinline__ uint32_t m_ge_f0(uint32_t x) { return m_ge_e0(x) & (x << 3); }
-
-// Gathers bit 7 of each byte lane into a 4-bit nibble (lane k -> bit k).
-__device__ __forceinline__ uint32_t gather4(uint32_t m) {
-  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
-}
-
-// Leads whose value range needs the second byte (C0 C1 E0 ED F0 F4..FF).
-// The low nibble of every lane is looked up in two 16-entry tables with one
-// PRMT each: entries 0..7 are table bytes, entries 8..15 replicate the sign
-// bit of entry k-8 (PRMT's sign-extend selector mode).
-__device__ __forceinline__ uint32_t m_special_lead(uint32_t x, uint32_t ge_c0, uint32_t ge_e0,
-                                                   uint32_t ge_f0) {
-  const uint32_t t = x & 0x0F0F0F0Fu;
-  const uint32_t u = t | (t >> 4);
-  const uint32_t sel = prmt(u, 0, 0x7720) & 0xFFFFu;  // nibbles ln0 ln1 ln2 ln3
-  // E row: special at low nibble 0 (E0) and 13 (ED).  bit 0 of the entry.
-  const uint32_t e_tab = prmt(0x00000001u, 0x00008000u, sel) & 0x01010101u;
-  // F row: special at 0 (F0) and 4..15 (F4..FF).  bit 0 of the entry.
-  const uint32_t f_tab = prmt(0x80808081u, 0x81818181u, sel) & 0x01010101u;
-  // C/D row: only C0 and C1, i.e. bits 1..4 clear.
-  const uint32_t x1e = x & 0x1E1E1E1Eu;
-  const uint32_t c_zero = ~((x1e + 0x7F7F7F7Fu) | x1e) & 0x80808080u;  // lane == 0
-  const uint32_t row_c = ge_c0 & ~ge_e0, row_e = ge_e0 & ~ge_f0, row_f = ge_f0;
-  return (row_c & c_zero) | (row_e & (e_tab << 7)) | (row_f & (f_tab << 7));
-}
+constexpr uint32_t H = 0x80808080u;
 
 __device__ __forceinline__ unsigned leadlen(unsigned b) {
-  return b < 0x80u ? 1u : b < 0xC0u ? 1u : b < 0xE0u ? 2u : b < 0xF0u ? 3u : b < 0xF8u ? 4u : 1u;
+  return b < 0xC0u ? 1u : b < 0xE0u ? 2u : b < 0xF0u ? 3u : b < 0xF8u ? 4u : 1u;
 }
 
 // proj/src/codec_core.cpp:5-38 on a 4-byte window (bytes past the input are
@@ -92,196 +67,351 @@ __device__ __forceinline__ bool decode_ok(uint32_t v) {
   return cp >= lo && cp <= 0x10FFFFu && (cp < 0xD800u || cp > 0xDFFFu);
 }
 
-// Per-thread view of one row: 16 own bytes (w[0..3]) and 4 bytes either side.
-struct Window {
-  uint32_t pw, w[5];  // w[4] = next word
+// A thread's 64 bytes plus the word before and the word after.
+struct Words {
+  uint32_t w[K8_WPT + 2];  // w[0] = previous word, w[1..16] = own, w[17] = next
 };
 
-// Exact first error among the thread's 16 byte positions:
-// a non-continuation byte whose decode fails, or a continuation byte no lead
-// in the 3 bytes before it reaches.  `lo`/`hi` bound the in-input positions.
-__device__ __noinline__ unsigned first_error_rule_a(const Window& win, unsigned lo, unsigned hi) {
-  uint32_t buf[6] = {win.pw, win.w[0], win.w[1], win.w[2], win.w[3], win.w[4]};
-  auto byte_at = [&](int p) -> unsigned {  // p in [-4, 20)
-    const int q = p + 4;
-    return (buf[q >> 2] >> ((q & 3) * 8)) & 0xFFu;
-  };
+__device__ __forceinline__ unsigned byte_at(const Words& W, int p) {  // p in [-4, 68)
+  const int q = p + 4;
+  return (W.w[q >> 2] >> ((q & 3) * 8)) & 0xFFu;
+}
+
+// Byte-granular masked load of a thread's window (ends of the input only).
+__device__ __noinline__ void load_masked(const U8Args& a, long long v0, Words& W) {
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  for (int k = 0; k < K8_WPT + 2; k++) {
+    uint32_t x = 0;
+    for (int b = 0; b < 4; b++) {
+      const long long p = v0 - 4 + 4 * k + b;
+      if (p >= lo && p < hi) x |= (uint32_t)a.base[p] << (8 * b);
+    }
+    W.w[k] = x;
+  }
+}
+
+// Exact first error among positions [lo, hi) of the thread's bytes.  Rare
+// path: reloads the thread's window itself (byte loads), so the hot path keeps
+// its words in registers.
+__device__ __noinline__ unsigned first_error_rule_a(const U8Args& a, long long v0, unsigned lo,
+                                                    unsigned hi) {
+  Words W;
+  load_masked(a, v0, W);
   for (unsigned i = lo; i < hi; i++) {
-    const unsigned b = byte_at((int)i);
+    const unsigned b = byte_at(W, (int)i);
     if ((b & 0xC0u) == 0x80u) {
       bool covered = false;
-      for (int j = (int)i - 3; j < (int)i; j++) {
-        if (leadlen(byte_at(j)) > (unsigned)((int)i - j)) covered = true;
-      }
+      for (int j = (int)i - 3; j < (int)i; j++)
+        if (leadlen(byte_at(W, j)) > (unsigned)((int)i - j)) covered = true;
       if (!covered) return i;
-    } else {
-      const uint32_t v = byte_at((int)i) | (byte_at((int)i + 1) << 8) |
-                         (byte_at((int)i + 2) << 16) | (byte_at((int)i + 3) << 24);
+    } else if (b >= 0x80u) {
+      const uint32_t v = b | (byte_at(W, (int)i + 1) << 8) | (byte_at(W, (int)i + 2) << 16) |
+                         (byte_at(W, (int)i + 3) << 24);
       if (!decode_ok(v)) return i;
     }
   }
   return kNone;
 }
 
-struct RowInfo {
-  uint32_t lead;  // bit p: a character starts at position p (in input, before any error)
-  uint32_t four;  // bit p: that character is 4 bytes long (2 UTF-16 units)
-  uint32_t ascii_words;  // bit k: word k is 4 in-input ASCII bytes
+struct ClassOut {
+  unsigned units;  // UTF-16 units of characters starting here (transcode) / characters
+  unsigned chars;
+  bool viol;       // lead/continuation structure violated near our bytes
+  bool susp;       // a lead whose value range must be checked (C0 C1 E0 ED EE EF)
+  bool four;       // a 4-byte lead (or F8..FF) in our bytes
 };
 
-// Phase 1 for one row of one thread: masks and the thread-local first error.
-__device__ __forceinline__ unsigned classify(const Window& win, unsigned lo, unsigned hi,
-                                             RowInfo& ri) {
-  uint32_t c[5], l2[5], l3[5], l4[5];
-  const uint32_t pl2 = m_ge_c0(win.pw), pl3 = m_ge_e0(win.pw), pl4 = m_ge_f0(win.pw);
-#pragma unroll
-  for (int k = 0; k < 5; k++) {
-    c[k] = m_cont(win.w[k]);
-    l2[k] = m_ge_c0(win.w[k]);
-    l3[k] = m_ge_e0(win.w[k]);
-    l4[k] = m_ge_f0(win.w[k]);
-  }
-  uint32_t viol = 0, special = 0, lead = 0, four = 0, ascii = 0;
-#pragma unroll
-  for (int k = 0; k < 5; k++) {
-    const uint32_t p2 = k ? l2[k - 1] : pl2, p3 = k ? l3[k - 1] : pl3, p4 = k ? l4[k - 1] : pl4;
-    const uint32_t need = __funnelshift_l(p2, l2[k], 8) | __funnelshift_l(p3, l3[k], 16) |
-                          __funnelshift_l(p4, l4[k], 24);
-    uint32_t v = (need ^ c[k]) & 0x80808080u;
-    if (k == 4) v &= 0x00808080u;  // next word: only lanes that can blame our bytes
-    viol |= v;
-    if (k < 4) {
-      special |= gather4(m_special_lead(win.w[k], l2[k], l3[k], l4[k])) << (4 * k);
-      lead |= gather4(~c[k] & 0x80808080u) << (4 * k);
-      four |= gather4(l4[k]) << (4 * k);
-      if (hi_bits(win.w[k]) == 0) ascii |= 1u << k;
-    }
-  }
-  const uint32_t inmask = (hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
-  special &= inmask & lead;
-  unsigned err = kNone;
-  bool check = viol != 0;
-  if (special) {
-    // exact range check of the special leads
-    uint32_t s = special;
-    while (s) {
-      const unsigned p = __ffs(s) - 1;
-      s &= s - 1;
-      const unsigned k = p >> 2, sh = (p & 3) * 8;
-      uint32_t a = win.w[0], b = win.w[1];
-      if (k == 1) { a = win.w[1]; b = win.w[2]; }
-      if (k == 2) { a = win.w[2]; b = win.w[3]; }
-      if (k == 3) { a = win.w[3]; b = win.w[4]; }
-      if (!decode_ok(__funnelshift_r(a, b, sh))) check = true;
-    }
-  }
-  if (check) err = first_error_rule_a(win, lo, hi);
-  ri.lead = lead & inmask;
-  ri.four = four & inmask;
-  uint32_t aw = 0;
-#pragma unroll
-  for (int k = 0; k < 4; k++)
-    if ((ascii >> k) & 1u) aw |= (((inmask >> (4 * k)) & 0xFu) == 0xFu) ? (1u << k) : 0u;
-  ri.ascii_words = aw;
-  return err;
+// Suspicious leads of word x (bit 7 of each lane), see classify().
+__device__ __forceinline__ uint32_t susp_lanes(uint32_t x) {
+  const uint32_t x2 = x << 1;
+  const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
+  const uint32_t t = (x & 0x0F0F0F0Fu) + 0x03030303u;
+  const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
+  const uint32_t y = x & 0x1E1E1E1Eu;
+  const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
+  return z3 | z2;
 }
 
-// Decodes the characters starting in this row's bytes (bits of `lead`) and
-// stores their UTF-16 units to shared memory at `dst`.
-__device__ __forceinline__ void emit_row(const Window& win, const RowInfo& ri, uint16_t* dst) {
-  unsigned q = 0;
+// Interior load of a thread's window (16-byte vector loads + halo words).
+__device__ __forceinline__ void load_interior(const uint8_t* p, Words& W) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
-    const uint32_t x = win.w[k];
-    const uint32_t lw = (ri.lead >> (4 * k)) & 0xFu;
-    if ((ri.ascii_words >> k) & 1u) {
-      dst[q + 0] = (uint16_t)(x & 0xFF);
-      dst[q + 1] = (uint16_t)((x >> 8) & 0xFF);
-      dst[q + 2] = (uint16_t)((x >> 16) & 0xFF);
-      dst[q + 3] = (uint16_t)(x >> 24);
-      q += 4;
-      continue;
-    }
-    uint32_t m = lw;
+  for (int r = 0; r < 4; r++) {
+    const uint4 v = __ldg(q + r);
+    W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y; W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
+  }
+  W.w[0] = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
+  W.w[K8_WPT + 1] = __ldg(reinterpret_cast<const uint32_t*>(p + K8_BPT));
+}
+
+// Exact range check of every suspicious lead (interior tiles; reloads the
+// window, which is still in L1/L2); true if one is malformed.
+__device__ __noinline__ bool susp_fail(const uint8_t* p) {
+  Words W;
+  load_interior(p, W);
+  for (int k = 0; k < K8_WPT; k++) {
+    uint32_t m = susp_lanes(W.w[k + 1]);
     while (m) {
-      const unsigned lane = __ffs(m) - 1;
+      const unsigned lanebit = __ffs(m) - 1;  // 7, 15, 23 or 31
       m &= m - 1;
-      const uint32_t v = __funnelshift_r(x, win.w[k + 1], lane * 8);
-      const unsigned b0 = v & 0xFF, b1 = (v >> 8) & 0x3F, b2 = (v >> 16) & 0x3F, b3 = (v >> 24) & 0x3F;
-      unsigned cp;
-      if (b0 < 0x80u) {
-        cp = b0;
-      } else if (b0 < 0xE0u) {
-        cp = ((b0 & 0x1Fu) << 6) | b1;
-      } else if (b0 < 0xF0u) {
-        cp = ((b0 & 0x0Fu) << 12) | (b1 << 6) | b2;
-      } else {
-        cp = ((b0 & 0x07u) << 18) | (b1 << 12) | (b2 << 6) | b3;
-      }
-      if (cp < 0x10000u) {
-        dst[q++] = (uint16_t)cp;
-      } else {
-        const unsigned s = cp - 0x10000u;
+      const uint32_t v = __funnelshift_r(W.w[k + 1], W.w[k + 2], lanebit - 7);
+      if (!decode_ok(v)) return true;
+    }
+  }
+  return false;
+}
+
+// Phase A over the 16 own words (SWAR, no branches).
+__device__ __forceinline__ ClassOut classify(const Words& W) {
+  uint32_t p2, p3, p4;
+  {
+    const uint32_t x = W.w[0], x2 = x << 1;
+    p2 = x & x2 & H;
+    p3 = p2 & (x << 2);
+    p4 = p3 & (x << 3);
+  }
+  uint32_t viol = 0, susp = 0, ccont = 0, cfour = 0;
+#pragma unroll
+  for (int k = 1; k <= K8_WPT + 1; k++) {
+    const uint32_t x = W.w[k], x2 = x << 1;
+    const uint32_t c = x & ~x2 & H;
+    const uint32_t l2 = x & x2 & H;
+    const uint32_t l3 = l2 & (x << 2);
+    const uint32_t l4 = l3 & (x << 3);
+    const uint32_t need = __funnelshift_l(p2, l2, 8) | __funnelshift_l(p3, l3, 16) |
+                          __funnelshift_l(p4, l4, 24);
+    if (k <= K8_WPT) {
+      viol |= need ^ c;
+      // E0 ED EE EF: ((low nibble + 3) & 0xC) == 0 ; C0 C1: (x & 0x1E) == 0
+      const uint32_t t = (x & 0x0F0F0F0Fu) + 0x03030303u;
+      const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
+      const uint32_t y = x & 0x1E1E1E1Eu;
+      const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
+      susp |= z3 | z2;
+      ccont += c >> 7;
+      cfour += l4 >> 7;
+    } else {
+      viol |= (need ^ c) & 0x00808080u;  // next word: lanes that can blame our bytes
+    }
+    p2 = l2; p3 = l3; p4 = l4;
+  }
+  ClassOut o;
+  const unsigned nc = (ccont * 0x01010101u) >> 24, n4 = (cfour * 0x01010101u) >> 24;
+  o.chars = K8_BPT - nc;
+  o.units = o.chars + n4;
+  o.viol = viol != 0;
+  o.susp = susp != 0;
+  o.four = n4 != 0;
+  return o;
+}
+
+// ---- generic path (ends of the input, tiles with an error): rare, per byte --
+// Counts (units or characters) of the characters starting at positions
+// [lo, lim) of the thread's bytes; with `dst`, also writes their units.
+__device__ __noinline__ unsigned generic_chars(const U8Args& a, long long v0, unsigned lo,
+                                               unsigned lim, bool units, uint16_t* dst) {
+  Words W;
+  load_masked(a, v0, W);
+  unsigned q = 0;
+  for (unsigned p = lo; p < lim; p++) {
+    const unsigned b0 = byte_at(W, (int)p);
+    if ((b0 & 0xC0u) == 0x80u) continue;  // continuation
+    const unsigned b1 = byte_at(W, (int)p + 1) & 0x3F, b2 = byte_at(W, (int)p + 2) & 0x3F,
+                   b3 = byte_at(W, (int)p + 3) & 0x3F;
+    unsigned cp;
+    if (b0 < 0x80u) cp = b0;
+    else if (b0 < 0xE0u) cp = ((b0 & 0x1Fu) << 6) | b1;
+    else if (b0 < 0xF0u) cp = ((b0 & 0x0Fu) << 12) | (b1 << 6) | b2;
+    else cp = ((b0 & 0x07u) << 18) | (b1 << 12) | (b2 << 6) | b3;
+    if (!units) {
+      q++;
+    } else if (cp < 0x10000u) {
+      if (dst) dst[q] = (uint16_t)cp;
+      q++;
+    } else {
+      const unsigned s = cp - 0x10000u;
+      if (dst) {
         dst[q] = (uint16_t)(0xD800u + (s >> 10));
         dst[q + 1] = (uint16_t)(0xDC00u + (s & 0x3FFu));
-        q += 2;
       }
+      q += 2;
     }
+  }
+  return q;
+}
+
+// 4-byte leads whose value range needs the second byte: F0, F4..FF (only
+// F1..F3 are always in range).  Interior tiles; reloads the window.
+__device__ __noinline__ bool four_fail(const uint8_t* p) {
+  Words W;
+  load_interior(p, W);
+  for (int k = 1; k <= K8_WPT; k++) {
+    const uint32_t x = W.w[k];
+    const uint32_t l4 = x & (x << 1) & (x << 2) & (x << 3) & H;
+    const uint32_t ln = x & 0x0F0F0F0Fu;
+    const uint32_t nz = ln + 0x7F7F7F7Fu;                       // bit 7: ln != 0
+    const uint32_t lt4 = ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);   // bit 7: ln < 4
+    uint32_t m = l4 & ~(nz & lt4);
+    while (m) {
+      const unsigned lanebit = __ffs(m) - 1;
+      m &= m - 1;
+      if (!decode_ok(__funnelshift_r(x, W.w[k + 1], lanebit - 7))) return true;
+    }
+  }
+  return false;
+}
+
+// Branch-free decode of one word: lead-attributed byte planes of each
+// character's UTF-16 unit (BMP), plus, with kFour, the surrogate pair of
+// 4-byte characters.  Predicated 16-bit stores at the running offset q.
+template <bool kFour>
+__device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint16_t* dst, unsigned& q) {
+  const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
+  const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
+  const uint32_t c2 = c << 1;
+  const uint32_t ascii7 = ~c & H;                 // lanes < 0x80
+  const uint32_t lead7 = ~(c & ~c2) & H;          // lanes that start a character
+  const uint32_t ge_e0 = c & c2 & (c << 2) & H;   // 3-byte (or 4-byte) leads
+  const uint32_t m1 = (ascii7 >> 7) * 0xFFu;
+  const uint32_t m3 = (ge_e0 >> 7) * 0xFFu;
+  const uint32_t A = (n1 & m3) | (c & ~m3);       // 3-byte: 2nd byte; 2-byte: lead
+  const uint32_t B = (n2 & m3) | (n1 & ~m3);      // last byte of the character
+  const uint32_t lom = ((A << 6) & 0xC0C0C0C0u) | (B & 0x3F3F3F3Fu);
+  const uint32_t lo = (c & m1) | (lom & ~m1);
+  const uint32_t him = ((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3);
+  const uint32_t hi = him & ~m1;
+  uint32_t u01 = prmt(lo, hi, 0x5140), u23 = prmt(lo, hi, 0x7362);
+  if (!kFour) {
+    if (lead7 & 0x00000080u) { dst[q] = (uint16_t)u01; q++; }
+    if (lead7 & 0x00008000u) { dst[q] = (uint16_t)(u01 >> 16); q++; }
+    if (lead7 & 0x00800000u) { dst[q] = (uint16_t)u23; q++; }
+    if (lead7 & 0x80000000u) { dst[q] = (uint16_t)(u23 >> 16); q++; }
+  } else {
+    // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10), low = 0xDC00 | (cp & 0x3FF)
+    const uint32_t n3 = prmt(c, n, 0x6543);
+    const uint32_t four7 = ge_e0 & (c << 3);
+    const uint32_t m4 = (four7 >> 7) * 0xFFu;
+    const uint32_t X = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
+    const uint32_t c7 = c & 0x07070707u;
+    const uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
+    const uint32_t hs23 = prmt(X, c7, 0x7362) + 0xD7C0D7C0u;
+    const uint32_t lsl = ((n2 << 6) & 0xC0C0C0C0u) | (n3 & 0x3F3F3F3Fu);
+    const uint32_t lsh = ((n2 >> 2) & 0x03030303u) | 0xDCDCDCDCu;
+    const uint32_t ls01 = prmt(lsl, lsh, 0x5140), ls23 = prmt(lsl, lsh, 0x7362);
+    const uint32_t m4_01 = prmt(m4, 0, 0x1100), m4_23 = prmt(m4, 0, 0x3322);
+    u01 = (u01 & ~m4_01) | (hs01 & m4_01);
+    u23 = (u23 & ~m4_23) | (hs23 & m4_23);
+    if (lead7 & 0x00000080u) { dst[q] = (uint16_t)u01; q++; }
+    if (four7 & 0x00000080u) { dst[q] = (uint16_t)ls01; q++; }
+    if (lead7 & 0x00008000u) { dst[q] = (uint16_t)(u01 >> 16); q++; }
+    if (four7 & 0x00008000u) { dst[q] = (uint16_t)(ls01 >> 16); q++; }
+    if (lead7 & 0x00800000u) { dst[q] = (uint16_t)u23; q++; }
+    if (four7 & 0x00800000u) { dst[q] = (uint16_t)ls23; q++; }
+    if (lead7 & 0x80000000u) { dst[q] = (uint16_t)(u23 >> 16); q++; }
+    if (four7 & 0x80000000u) { dst[q] = (uint16_t)(ls23 >> 16); q++; }
   }
 }
 
-struct U8Smem {
-  alignas(16) uint8_t in[16 + U8_TILE + 16];
+struct K8Smem {
   alignas(16) uint8_t out_pad[32];
-  alignas(16) uint16_t out[U8_TILE];
+  alignas(16) uint16_t out[K8_TILE];
   alignas(16) uint8_t out_tail[32];
-  unsigned scan[U8_THREADS / 32];
-  unsigned red[U8_THREADS / 32];
+  unsigned scan[K8_THREADS / 32];
+  unsigned red[K8_THREADS / 32];
   unsigned long long excl;
   unsigned tile;
-  unsigned flag;
 };
 
-// Loads tile `tile` (16-byte chunks, zero outside the input) into smem.
-__device__ __forceinline__ void load_tile(const U8Args& a, unsigned tile, uint8_t* in_s) {
-  const unsigned long long vbase = (unsigned long long)tile * U8_TILE;  // virtual byte of in_s[16]
-  const unsigned long long vend = a.head + a.n;
-  for (int j = threadIdx.x; j < U8_TILE / 16 + 2; j += U8_THREADS) {
-    const long long vc = (long long)vbase - 16 + 16LL * j;  // virtual start of chunk
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (vc >= 0 && (unsigned long long)vc < vend && (unsigned long long)vc + 16 > a.head) {
-      v = __ldcs(reinterpret_cast<const uint4*>(a.base + vc));
-      if ((unsigned long long)vc < a.head || (unsigned long long)vc + 16 > vend) {
-        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+template <bool kTranscode>
+__device__ __forceinline__ void process_tile(const U8Args& a, unsigned tile, K8Smem& sm) {
+  const unsigned lane = threadIdx.x & 31;
+  const long long vt0 = (long long)tile * K8_TILE;             // virtual start of the tile
+  const long long v0 = vt0 + (long long)K8_BPT * threadIdx.x;  // this thread's bytes
+  // interior: the tile and both halo words lie inside the input
+  const bool interior =
+      vt0 - 4 >= (long long)a.head && vt0 + K8_TILE + 4 <= (long long)(a.head + a.n);
+  Words W;
+  if (interior) {
+    const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
 #pragma unroll
-        for (int b = 0; b < 16; b++) {
-          const unsigned long long pos = (unsigned long long)vc + b;
-          if (pos < a.head || pos >= vend) w[b >> 2] &= ~(0xFFu << ((b & 3) * 8));
-        }
-        v = make_uint4(w[0], w[1], w[2], w[3]);
-      }
+    for (int r = 0; r < 4; r++) {
+      const uint4 v = __ldg(p + r);
+      W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y; W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
     }
-    *reinterpret_cast<uint4*>(in_s + 16 * j) = v;
+    uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K8_WPT], 1);
+    uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
+    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 4));
+    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K8_BPT));
+    W.w[0] = pw;
+    W.w[K8_WPT + 1] = nw;
+  } else {
+    Words L;
+    load_masked(a, v0, L);
+#pragma unroll
+    for (int k = 0; k < K8_WPT + 2; k++) W.w[k] = L.w[k];
   }
-}
-
-__device__ __forceinline__ void thread_bounds(const U8Args& a, unsigned tile, int row,
-                                              unsigned& lo, unsigned& hi) {
-  const long long v0 = (long long)tile * U8_TILE + row * U8_ROW + 16 * threadIdx.x;
+  // in-input positions of this thread's bytes
   const long long s = (long long)a.head - v0, e = (long long)(a.head + a.n) - v0;
-  lo = (unsigned)max(0LL, min(16LL, s));
-  hi = (unsigned)max(0LL, min(16LL, e));
-  if (hi < lo) hi = lo;
-}
+  const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
+  const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, e));
 
-__device__ __forceinline__ Window load_window(const uint8_t* in_s, int row) {
-  const uint8_t* p = in_s + 16 + row * U8_ROW + 16 * threadIdx.x;
-  Window w;
-  const uint4 v = *reinterpret_cast<const uint4*>(p);
-  w.pw = *reinterpret_cast<const uint32_t*>(p - 4);
-  w.w[0] = v.x; w.w[1] = v.y; w.w[2] = v.z; w.w[3] = v.w;
-  w.w[4] = *reinterpret_cast<const uint32_t*>(p + 16);
-  return w;
+  const ClassOut co = classify(W);
+  unsigned my_err = kNone;
+  if (co.viol || !interior || (co.susp && susp_fail(a.base + v0)) ||
+      (co.four && four_fail(a.base + v0))) {
+    const unsigned er = first_error_rule_a(a, v0, lo, hi);
+    if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
+  }
+  const unsigned tile_err = block_min<K8_THREADS>(my_err, sm.red);
+  const bool simple = interior && tile_err == kNone;
+  unsigned lim = hi;
+  if (tile_err != kNone) {
+    const unsigned start = K8_BPT * threadIdx.x;
+    lim = max(lo, min(lim, tile_err <= start ? 0u : tile_err - start));
+  }
+  const unsigned cnt = simple ? (kTranscode ? co.units : co.chars)
+                              : generic_chars(a, v0, lo, lim, kTranscode, nullptr);
+  if (tile_err != kNone && threadIdx.x == 0) {
+    const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
+    atomicMin(&a.ctl->err, pos);
+  }
+  unsigned agg;
+  const unsigned off = block_excl_scan<K8_THREADS>(cnt, sm.scan, agg);
+  if (!kTranscode) {
+    if (threadIdx.x == 0 && agg) atomicAdd(&a.ctl->count, (unsigned long long)agg);
+    return;
+  }
+  // publish the aggregate, resolve the exclusive prefix (warp 0)
+  if (threadIdx.x < 32) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      if (threadIdx.x == 0) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
+    } else {
+      if (threadIdx.x == 0) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
+      excl = lookback(a.status, a.epoch, tile, a.ctl, K8_TILE, a.head);
+      if (threadIdx.x == 0 && excl != ~0ull)
+        store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
+    }
+    if (threadIdx.x == 0) sm.excl = excl;
+  }
+  uint16_t* dst = sm.out + off;
+  if (simple) {
+    unsigned q = 0;
+    if (!co.four) {
+#pragma unroll
+      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(W.w[k], W.w[k + 1], dst, q);
+    } else {
+#pragma unroll
+      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(W.w[k], W.w[k + 1], dst, q);
+    }
+  } else {
+    generic_chars(a, v0, lo, lim, true, dst);
+  }
+  __syncthreads();
+  const unsigned long long excl = sm.excl;
+  if (excl != ~0ull)
+    copy_out(reinterpret_cast<uint8_t*>(a.out + excl), reinterpret_cast<const uint8_t*>(sm.out),
+             2u * agg);
 }
 
 __device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode) {
@@ -294,14 +424,8 @@ __device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode
       const unsigned long long e = load_relaxed(&a.ctl->err);
       vt_result r;
       if (transcode) {
-        unsigned long long written;
-        if (e == kNoError) {
-          written = load_status(&a.status[a.ntiles - 1]) & kValMask;
-        } else {
-          const unsigned et = (unsigned)((e + a.head) / U8_TILE);
-          written = load_status(&a.status[et]) & kValMask;
-        }
-        r.written = written;
+        const unsigned t = e == kNoError ? a.ntiles - 1 : (unsigned)((e + a.head) / K8_TILE);
+        r.written = load_status(&a.status[t]) & kValMask;
       } else {
         r.written = load_relaxed(&a.ctl->count);
       }
@@ -318,90 +442,20 @@ __device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode
 }
 
 template <bool kTranscode>
-__global__ void __launch_bounds__(U8_THREADS) utf8_kernel(U8Args a) {
-  __shared__ U8Smem sm;
+__global__ void __launch_bounds__(K8_THREADS, 4) utf8_kernel(U8Args a) {
+  __shared__ K8Smem sm;
   while (true) {
     if (threadIdx.x == 0) {
       unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
       const unsigned long long e = load_relaxed(&a.ctl->err);
       // tiles behind a known error never matter: stop (the reference stops too)
-      if (t < a.ntiles && e != kNoError && (e + a.head) / U8_TILE < t) t = a.ntiles;
+      if (t < a.ntiles && e != kNoError && (e + a.head) / K8_TILE < t) t = a.ntiles;
       sm.tile = t;
     }
     __syncthreads();
     const unsigned tile = sm.tile;
     if (tile >= a.ntiles) break;
-
-    load_tile(a, tile, sm.in);
-    __syncthreads();
-
-    Window win[U8_ROWS];
-    RowInfo ri[U8_ROWS];
-    unsigned lo[U8_ROWS], hi[U8_ROWS];
-    unsigned my_err = kNone;
-#pragma unroll
-    for (int r = 0; r < U8_ROWS; r++) {
-      win[r] = load_window(sm.in, r);
-      thread_bounds(a, tile, r, lo[r], hi[r]);
-      const unsigned e = classify(win[r], lo[r], hi[r], ri[r]);
-      if (e != kNone && my_err == kNone) my_err = r * U8_ROW + 16 * threadIdx.x + e;
-    }
-    const unsigned tile_err = block_min<U8_THREADS>(my_err, sm.red);
-    // keep only characters before the tile's first error
-    unsigned cnt[U8_ROWS];
-#pragma unroll
-    for (int r = 0; r < U8_ROWS; r++) {
-      const unsigned start = r * U8_ROW + 16 * threadIdx.x;
-      if (tile_err != kNone) {
-        const unsigned lim = tile_err <= start ? 0u : min(16u, tile_err - start);
-        const uint32_t keep = lim >= 32 ? 0xFFFFFFFFu : ((1u << lim) - 1u);
-        ri[r].lead &= keep;
-        ri[r].four &= keep;
-        uint32_t aw = 0;
-        for (int k = 0; k < 4; k++)
-          if (((ri[r].ascii_words >> k) & 1u) && ((keep >> (4 * k)) & 0xFu) == 0xFu) aw |= 1u << k;
-        ri[r].ascii_words = aw;
-      }
-      cnt[r] = kTranscode ? __popc(ri[r].lead) + __popc(ri[r].four) : __popc(ri[r].lead);
-    }
-    if (tile_err != kNone && threadIdx.x == 0) {
-      const unsigned long long pos = (unsigned long long)tile * U8_TILE + tile_err - a.head;
-      atomicMin(&a.ctl->err, pos);
-    }
-
-    if (!kTranscode) {
-      unsigned total;
-      block_excl_scan<U8_THREADS>(cnt[0] + cnt[1], sm.scan, total);
-      if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
-      __syncthreads();
-      continue;
-    }
-
-    unsigned tot0, tot1;
-    const unsigned off0 = block_excl_scan<U8_THREADS>(cnt[0], sm.scan, tot0);
-    const unsigned off1 = block_excl_scan<U8_THREADS>(cnt[1], sm.scan, tot1) + tot0;
-    const unsigned agg = tot0 + tot1;
-
-    // publish the aggregate, then resolve the exclusive prefix
-    if (threadIdx.x < 32) {
-      unsigned long long excl = 0;
-      if (tile == 0) {
-        if (threadIdx.x == 0) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
-      } else {
-        if (threadIdx.x == 0) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
-        excl = lookback(a.status, a.epoch, tile, a.ctl, U8_TILE, a.head);
-        if (threadIdx.x == 0 && excl != ~0ull)
-          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
-      }
-      if (threadIdx.x == 0) sm.excl = excl;
-    }
-    emit_row(win[0], ri[0], sm.out + off0);
-    emit_row(win[1], ri[1], sm.out + off1);
-    __syncthreads();
-    const unsigned long long excl = sm.excl;
-    if (excl != ~0ull)
-      copy_out(reinterpret_cast<uint8_t*>(a.out + excl), reinterpret_cast<const uint8_t*>(sm.out),
-               2u * agg);
+    process_tile<kTranscode>(a, tile, sm);
     __syncthreads();
   }
   finalize_if_last(a, kTranscode);
@@ -409,23 +463,23 @@ __global__ void __launch_bounds__(U8_THREADS) utf8_kernel(U8Args a) {
 
 int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s) {
   if (transcode)
-    utf8_kernel<true><<<grid, U8_THREADS, 0, s>>>(a);
+    utf8_kernel<true><<<grid, K8_THREADS, 0, s>>>(a);
   else
-    utf8_kernel<false><<<grid, U8_THREADS, 0, s>>>(a);
+    utf8_kernel<false><<<grid, K8_THREADS, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int occupancy_utf8(bool transcode) {
   int n = 0;
   if (transcode)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<true>, U8_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<true>, K8_THREADS, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<false>, U8_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<false>, K8_THREADS, 0);
   return n;
 }
 
 unsigned tiles_utf8(unsigned long long head, unsigned long long n) {
-  const unsigned long long t = (head + n + U8_TILE - 1) / U8_TILE;
+  const unsigned long long t = (head + n + K8_TILE - 1) / K8_TILE;
   return (unsigned)(t ? t : 1);
 }
 
