@@ -265,7 +265,7 @@ __device__ __noinline__ bool four_fail(const uint8_t* p) {
 // character's UTF-16 unit (BMP), plus, with kFour, the surrogate pair of
 // 4-byte characters.  Predicated 16-bit stores at the running offset q.
 template <bool kFour>
-__device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint16_t* dst, unsigned& q) {
+__device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
   const uint32_t c2 = c << 1;
@@ -282,10 +282,10 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint16_t* dst,
   const uint32_t hi = him & ~m1;
   uint32_t u01 = prmt(lo, hi, 0x5140), u23 = prmt(lo, hi, 0x7362);
   if (!kFour) {
-    if (lead7 & 0x00000080u) { dst[q] = (uint16_t)u01; q++; }
-    if (lead7 & 0x00008000u) { dst[q] = (uint16_t)(u01 >> 16); q++; }
-    if (lead7 & 0x00800000u) { dst[q] = (uint16_t)u23; q++; }
-    if (lead7 & 0x80000000u) { dst[q] = (uint16_t)(u23 >> 16); q++; }
+    if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
+    if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
+    if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
+    if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
   } else {
     // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10), low = 0xDC00 | (cp & 0x3FF)
     const uint32_t n3 = prmt(c, n, 0x6543);
@@ -301,14 +301,14 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint16_t* dst,
     const uint32_t m4_01 = prmt(m4, 0, 0x1100), m4_23 = prmt(m4, 0, 0x3322);
     u01 = (u01 & ~m4_01) | (hs01 & m4_01);
     u23 = (u23 & ~m4_23) | (hs23 & m4_23);
-    if (lead7 & 0x00000080u) { dst[q] = (uint16_t)u01; q++; }
-    if (four7 & 0x00000080u) { dst[q] = (uint16_t)ls01; q++; }
-    if (lead7 & 0x00008000u) { dst[q] = (uint16_t)(u01 >> 16); q++; }
-    if (four7 & 0x00008000u) { dst[q] = (uint16_t)(ls01 >> 16); q++; }
-    if (lead7 & 0x00800000u) { dst[q] = (uint16_t)u23; q++; }
-    if (four7 & 0x00800000u) { dst[q] = (uint16_t)ls23; q++; }
-    if (lead7 & 0x80000000u) { dst[q] = (uint16_t)(u23 >> 16); q++; }
-    if (four7 & 0x80000000u) { dst[q] = (uint16_t)(ls23 >> 16); q++; }
+    if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
+    if (four7 & 0x00000080u) { sts16(q, ls01); q += 2; }
+    if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
+    if (four7 & 0x00008000u) { sts16(q, (ls01 >> 16)); q += 2; }
+    if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
+    if (four7 & 0x00800000u) { sts16(q, ls23); q += 2; }
+    if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
+    if (four7 & 0x80000000u) { sts16(q, (ls23 >> 16)); q += 2; }
   }
 }
 
@@ -394,18 +394,17 @@ __device__ __forceinline__ void process_tile(const U8Args& a, unsigned tile, K8S
     }
     if (threadIdx.x == 0) sm.excl = excl;
   }
-  uint16_t* dst = sm.out + off;
   if (simple) {
-    unsigned q = 0;
+    uint32_t q = smem_addr(sm.out) + 2u * off;
     if (!co.four) {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(W.w[k], W.w[k + 1], dst, q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(W.w[k], W.w[k + 1], q);
     } else {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(W.w[k], W.w[k + 1], dst, q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(W.w[k], W.w[k + 1], q);
     }
   } else {
-    generic_chars(a, v0, lo, lim, true, dst);
+    generic_chars(a, v0, lo, lim, true, sm.out + off);
   }
   __syncthreads();
   const unsigned long long excl = sm.excl;
@@ -445,6 +444,8 @@ template <bool kTranscode>
 __global__ void __launch_bounds__(K8_THREADS, 4) utf8_kernel(U8Args a) {
   __shared__ K8Smem sm;
   while (true) {
+    // Tiles are taken in order, one at a time: a CTA only holds a tile it is
+    // working on, so look-back never waits for a tile nobody has started.
     if (threadIdx.x == 0) {
       unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
       const unsigned long long e = load_relaxed(&a.ctl->err);

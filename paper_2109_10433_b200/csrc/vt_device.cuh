@@ -31,6 +31,23 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// Shared-memory accesses through 32-bit shared-window addresses (a generic
+// pointer into shared memory costs an address conversion per access).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)(v & 0xFF)));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
 // Per-call control block.  Zeroed once at allocation; the finalising CTA of
 // every launch re-arms it, so consecutive calls on one stream need no memset.
 struct Ctl {
@@ -118,29 +135,26 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 
 // Copies `len` bytes from shared memory `src` (16-byte aligned) to global `dst`
 // (any alignment) with aligned 16-byte stores in the body.  The whole CTA
-// participates.  `src` must have >= 16 readable bytes before and after.
+// participates.  `src` must have >= 16 readable bytes before and >= 20 after.
 __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
                                          unsigned len) {
   if (len == 0) return;
-  const uintptr_t d0 = (uintptr_t)dst;
-  const unsigned mis = (unsigned)(d0 & 15);  // dst chunk c covers src bytes [16c - mis, 16c - mis + 16)
+  const unsigned mis = (unsigned)((uintptr_t)dst & 15);  // chunk c <- src[16c - mis, +16)
   const unsigned nchunks = (mis + len + 15) >> 4;
   uint8_t* dbase = dst - mis;
-  const unsigned ws = (16 - mis) & 15;  // source offset of chunk c is 16c - mis = 16(c-1) + ws
+  const uint32_t sbase = smem_addr(src);
+  // the byte shift inside a word is the same for every chunk
+  const unsigned bs = ((16u - mis) & 3u) * 8u;
   for (unsigned c = threadIdx.x; c < nchunks; c += blockDim.x) {
-    // gather 16 source bytes starting at src + 16c - mis
     const int so = (int)(16 * c) - (int)mis;
-    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src + ((so >> 2) << 2) - 0);
-    uint32_t w[5];
-    // so may be negative for c == 0 (the first chunk); src has >= 16 bytes of slack before
-#pragma unroll
-    for (int i = 0; i < 5; i++) w[i] = s32[i];
-    const unsigned bs = (unsigned)(so & 3) * 8;
+    const uint32_t a = sbase + (uint32_t)((so >> 2) << 2);
+    const uint32_t w0 = lds32(a), w1 = lds32(a + 4), w2 = lds32(a + 8), w3 = lds32(a + 12),
+                   w4 = lds32(a + 16);
     uint4 v;
-    v.x = __funnelshift_r(w[0], w[1], bs);
-    v.y = __funnelshift_r(w[1], w[2], bs);
-    v.z = __funnelshift_r(w[2], w[3], bs);
-    v.w = __funnelshift_r(w[3], w[4], bs);
+    v.x = __funnelshift_r(w0, w1, bs);
+    v.y = __funnelshift_r(w1, w2, bs);
+    v.z = __funnelshift_r(w2, w3, bs);
+    v.w = __funnelshift_r(w3, w4, bs);
     uint8_t* d = dbase + 16 * c;
     const bool full = (c > 0 || mis == 0) && (16 * c + 16 <= mis + len);
     if (full) {
@@ -154,7 +168,6 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
       }
     }
   }
-  (void)ws;
 }
 
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).
