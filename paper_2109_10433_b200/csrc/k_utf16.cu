@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(U16_THREADS) utf16_kernel(U16Args a) {
     }
     __syncthreads();
     const unsigned long long excl = sm.excl;
-    if (excl != ~0ull) copy_out(a.out + excl, sm.out, agg);
+    if (excl != ~0ull) copy_out(a.out + excl, sm.out, agg, U16_THREADS);
     __syncthreads();
   }
   // last CTA writes the result and re-arms the control block

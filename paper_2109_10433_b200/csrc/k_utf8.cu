@@ -312,105 +312,86 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   }
 }
 
-struct K8Smem {
-  alignas(16) uint8_t out_pad[32];
-  alignas(16) uint16_t out[K8_TILE];
-  alignas(16) uint8_t out_tail[32];
-  unsigned scan[K8_THREADS / 32];
-  unsigned red[K8_THREADS / 32];
-  unsigned long long excl;
-  unsigned tile;
+// ---- per-tile front half: load, classify, locate errors, count -------------
+struct TileCount {
+  Words W;
+  long long v0;
+  unsigned lo, lim;  // in-input positions [lo, lim) of the thread (clipped at the tile's error)
+  bool simple;       // interior tile without error: SWAR emission from W
+  bool four;         // the thread has 4-byte characters
+  unsigned cnt;      // units (transcode) or characters of the thread
 };
 
-template <bool kTranscode>
-__device__ __forceinline__ void process_tile(const U8Args& a, unsigned tile, K8Smem& sm) {
+template <bool kTranscode, int NT, class Sync>
+__device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsigned* red,
+                                           unsigned& tile_err, TileCount& tc) {
   const unsigned lane = threadIdx.x & 31;
-  const long long vt0 = (long long)tile * K8_TILE;             // virtual start of the tile
-  const long long v0 = vt0 + (long long)K8_BPT * threadIdx.x;  // this thread's bytes
+  const long long vt0 = (long long)tile * K8_TILE;  // virtual start of the tile
+  tc.v0 = vt0 + (long long)K8_BPT * threadIdx.x;
   // interior: the tile and both halo words lie inside the input
   const bool interior =
       vt0 - 4 >= (long long)a.head && vt0 + K8_TILE + 4 <= (long long)(a.head + a.n);
-  Words W;
   if (interior) {
-    const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
+    const uint4* p = reinterpret_cast<const uint4*>(a.base + tc.v0);
 #pragma unroll
     for (int r = 0; r < 4; r++) {
       const uint4 v = __ldg(p + r);
-      W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y; W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
+      tc.W.w[1 + 4 * r] = v.x; tc.W.w[2 + 4 * r] = v.y;
+      tc.W.w[3 + 4 * r] = v.z; tc.W.w[4 + 4 * r] = v.w;
     }
-    uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K8_WPT], 1);
-    uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
-    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 4));
-    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K8_BPT));
-    W.w[0] = pw;
-    W.w[K8_WPT + 1] = nw;
+    uint32_t pw = __shfl_up_sync(0xffffffffu, tc.W.w[K8_WPT], 1);
+    uint32_t nw = __shfl_down_sync(0xffffffffu, tc.W.w[1], 1);
+    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 - 4));
+    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 + K8_BPT));
+    tc.W.w[0] = pw;
+    tc.W.w[K8_WPT + 1] = nw;
   } else {
     Words L;
-    load_masked(a, v0, L);
+    load_masked(a, tc.v0, L);
 #pragma unroll
-    for (int k = 0; k < K8_WPT + 2; k++) W.w[k] = L.w[k];
+    for (int k = 0; k < K8_WPT + 2; k++) tc.W.w[k] = L.w[k];
   }
-  // in-input positions of this thread's bytes
-  const long long s = (long long)a.head - v0, e = (long long)(a.head + a.n) - v0;
-  const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
-  const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, e));
-
-  const ClassOut co = classify(W);
+  const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
+  tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
+  const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
+  const ClassOut co = classify(tc.W);
   unsigned my_err = kNone;
-  if (co.viol || !interior || (co.susp && susp_fail(a.base + v0)) ||
-      (co.four && four_fail(a.base + v0))) {
-    const unsigned er = first_error_rule_a(a, v0, lo, hi);
+  if (co.viol || !interior || (co.susp && susp_fail(a.base + tc.v0)) ||
+      (co.four && four_fail(a.base + tc.v0))) {
+    const unsigned er = first_error_rule_a(a, tc.v0, tc.lo, hi);
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
-  const unsigned tile_err = block_min<K8_THREADS>(my_err, sm.red);
-  const bool simple = interior && tile_err == kNone;
-  unsigned lim = hi;
+  tile_err = block_min<NT, Sync>(my_err, red);
+  tc.simple = interior && tile_err == kNone;
+  tc.four = co.four;
+  tc.lim = hi;
   if (tile_err != kNone) {
     const unsigned start = K8_BPT * threadIdx.x;
-    lim = max(lo, min(lim, tile_err <= start ? 0u : tile_err - start));
+    tc.lim = max(tc.lo, min(hi, tile_err <= start ? 0u : tile_err - start));
   }
-  const unsigned cnt = simple ? (kTranscode ? co.units : co.chars)
-                              : generic_chars(a, v0, lo, lim, kTranscode, nullptr);
+  tc.cnt = tc.simple ? (kTranscode ? co.units : co.chars)
+                     : generic_chars(a, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
   if (tile_err != kNone && threadIdx.x == 0) {
     const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
     atomicMin(&a.ctl->err, pos);
   }
-  unsigned agg;
-  const unsigned off = block_excl_scan<K8_THREADS>(cnt, sm.scan, agg);
-  if (!kTranscode) {
-    if (threadIdx.x == 0 && agg) atomicAdd(&a.ctl->count, (unsigned long long)agg);
-    return;
-  }
-  // publish the aggregate, resolve the exclusive prefix (warp 0)
-  if (threadIdx.x < 32) {
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      if (threadIdx.x == 0) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
-    } else {
-      if (threadIdx.x == 0) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
-      excl = lookback(a.status, a.epoch, tile, a.ctl, K8_TILE, a.head);
-      if (threadIdx.x == 0 && excl != ~0ull)
-        store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
-    }
-    if (threadIdx.x == 0) sm.excl = excl;
-  }
-  if (simple) {
-    uint32_t q = smem_addr(sm.out) + 2u * off;
-    if (!co.four) {
+}
+
+// ---- per-tile back half: decode into the staging buffer -----------------------
+__device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
+                                          unsigned off) {
+  if (tc.simple) {
+    uint32_t q = smem_addr(stage) + 2u * off;
+    if (!tc.four) {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(W.w[k], W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(W.w[k], W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(tc.W.w[k], tc.W.w[k + 1], q);
     }
   } else {
-    generic_chars(a, v0, lo, lim, true, sm.out + off);
+    generic_chars(a, tc.v0, tc.lo, tc.lim, true, stage + off);
   }
-  __syncthreads();
-  const unsigned long long excl = sm.excl;
-  if (excl != ~0ull)
-    copy_out(reinterpret_cast<uint8_t*>(a.out + excl), reinterpret_cast<const uint8_t*>(sm.out),
-             2u * agg);
 }
 
 __device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode) {
@@ -440,42 +421,146 @@ __device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode
   }
 }
 
-template <bool kTranscode>
-__global__ void __launch_bounds__(K8_THREADS, 4) utf8_kernel(U8Args a) {
-  __shared__ K8Smem sm;
+// Next tile for this CTA (thread 0).  Tiles are taken in order, one at a time
+// per CTA, so look-back never waits for a tile nobody has started; tiles
+// behind a known error are skipped (the reference stops there too).
+__device__ __forceinline__ unsigned grab_tile(const U8Args& a) {
+  unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
+  const unsigned long long e = load_relaxed(&a.ctl->err);
+  if (t < a.ntiles && e != kNoError && (e + a.head) / K8_TILE < t) t = a.ntiles;
+  return t;
+}
+
+// ---- validation / counting: no output, no look-back -----------------------------
+__global__ void __launch_bounds__(K8_THREADS, 4) utf8_validate_kernel(U8Args a) {
+  __shared__ unsigned red[K8_THREADS / 32], scan[K8_THREADS / 32];
+  __shared__ unsigned tile_s;
   while (true) {
-    // Tiles are taken in order, one at a time: a CTA only holds a tile it is
-    // working on, so look-back never waits for a tile nobody has started.
-    if (threadIdx.x == 0) {
-      unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
-      const unsigned long long e = load_relaxed(&a.ctl->err);
-      // tiles behind a known error never matter: stop (the reference stops too)
-      if (t < a.ntiles && e != kNoError && (e + a.head) / K8_TILE < t) t = a.ntiles;
-      sm.tile = t;
-    }
+    if (threadIdx.x == 0) tile_s = grab_tile(a);
     __syncthreads();
-    const unsigned tile = sm.tile;
+    const unsigned tile = tile_s;
     if (tile >= a.ntiles) break;
-    process_tile<kTranscode>(a, tile, sm);
-    __syncthreads();
+    TileCount tc;
+    unsigned tile_err;
+    count_tile<false, K8_THREADS, SyncAll>(a, tile, red, tile_err, tc);
+    unsigned total;
+    block_excl_scan<K8_THREADS>(tc.cnt, scan, total);
+    if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
   }
-  finalize_if_last(a, kTranscode);
+  finalize_if_last(a, false);
+}
+
+// ---- transcoding: warp-specialised pipeline ----------------------------------------
+// Warps 0..7 (compute) count tile j, hand its aggregate to warp 8 (look-back),
+// decode it into staging buffer j%2, and copy tile j-1 out once warp 8 has
+// resolved its offset.  The look-back latency is hidden behind a whole tile.
+constexpr int K8_BLOCK = K8_THREADS + 32;
+constexpr int BAR_COMPUTE = 1, BAR_AGG = 2, BAR_EXCL = 3;
+constexpr unsigned kSentinel = 0xFFFFFFFFu;
+using ComputeSync = SyncNamed<BAR_COMPUTE, K8_THREADS>;
+
+struct K8TSmem {
+  alignas(16) uint8_t pad0[32];
+  alignas(16) uint16_t out[2][K8_TILE + 16];
+  alignas(16) uint8_t pad1[32];
+  unsigned scan[K8_THREADS / 32];
+  unsigned red[K8_THREADS / 32];
+  unsigned tile;
+  unsigned agg_tile[2], agg[2];
+  unsigned long long excl[2];
+};
+
+__global__ void __launch_bounds__(K8_BLOCK, 3) utf8_transcode_kernel(U8Args a) {
+  extern __shared__ __align__(16) uint8_t k8_dyn_smem[];
+  K8TSmem& sm = *reinterpret_cast<K8TSmem*>(k8_dyn_smem);
+  if (threadIdx.x >= K8_THREADS) {
+    // look-back warp
+    for (unsigned j = 0;; j++) {
+      bar_sync(BAR_AGG, K8_BLOCK);
+      const unsigned tile = sm.agg_tile[j & 1];
+      if (tile == kSentinel) break;
+      const unsigned agg = sm.agg[j & 1];
+      unsigned long long excl = 0;
+      if (tile == 0) {
+        if (threadIdx.x == K8_THREADS) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
+      } else {
+        if (threadIdx.x == K8_THREADS)
+          store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
+        excl = lookback(a.status, a.epoch, tile, a.ctl, K8_TILE, a.head);
+        if (threadIdx.x == K8_THREADS && excl != ~0ull)
+          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
+      }
+      if (threadIdx.x == K8_THREADS) sm.excl[j & 1] = excl;
+      __syncwarp();
+      bar_arrive(BAR_EXCL, K8_BLOCK);
+    }
+  } else {
+    // compute warps
+    if (threadIdx.x == 0) sm.tile = grab_tile(a);
+    unsigned j = 0, prev_agg = 0;
+    while (true) {
+      ComputeSync::sync();
+      const unsigned tile = sm.tile;
+      if (tile >= a.ntiles) break;
+      TileCount tc;
+      unsigned tile_err, agg;
+      count_tile<true, K8_THREADS, ComputeSync>(a, tile, sm.red, tile_err, tc);
+      const unsigned off = block_excl_scan<K8_THREADS, ComputeSync>(tc.cnt, sm.scan, agg);
+      if (j > 0) {
+        // tile j-1: wait for its offset, then copy it out
+        bar_sync(BAR_EXCL, K8_BLOCK);
+        const unsigned long long excl = sm.excl[(j - 1) & 1];
+        if (excl != ~0ull)
+          copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
+                   reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
+      }
+      if (threadIdx.x == 0) {
+        sm.agg_tile[j & 1] = tile;
+        sm.agg[j & 1] = agg;
+      }
+      bar_arrive(BAR_AGG, K8_BLOCK);
+      emit_tile(a, tc, sm.out[j & 1], off);
+      if (threadIdx.x == 0) sm.tile = grab_tile(a);
+      prev_agg = agg;
+      j++;
+    }
+    if (j > 0) {
+      bar_sync(BAR_EXCL, K8_BLOCK);
+      const unsigned long long excl = sm.excl[(j - 1) & 1];
+      if (excl != ~0ull)
+        copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
+                 reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
+    }
+    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
+    bar_arrive(BAR_AGG, K8_BLOCK);
+  }
+  finalize_if_last(a, true);
+}
+
+static int set_smem_attr() {
+  return (int)cudaFuncSetAttribute(utf8_transcode_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K8TSmem));
 }
 
 int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s) {
+  static const int attr_rc = set_smem_attr();
+  if (attr_rc) return attr_rc;
   if (transcode)
-    utf8_kernel<true><<<grid, K8_THREADS, 0, s>>>(a);
+    utf8_transcode_kernel<<<grid, K8_BLOCK, sizeof(K8TSmem), s>>>(a);
   else
-    utf8_kernel<false><<<grid, K8_THREADS, 0, s>>>(a);
+    utf8_validate_kernel<<<grid, K8_THREADS, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int occupancy_utf8(bool transcode) {
   int n = 0;
-  if (transcode)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<true>, K8_THREADS, 0);
+  if (transcode) {
+    if (set_smem_attr()) return 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel, K8_BLOCK,
+                                                  sizeof(K8TSmem));
+  }
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_kernel<false>, K8_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel, K8_THREADS, 0);
   return n;
 }
 

@@ -134,10 +134,11 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 }
 
 // Copies `len` bytes from shared memory `src` (16-byte aligned) to global `dst`
-// (any alignment) with aligned 16-byte stores in the body.  The whole CTA
-// participates.  `src` must have >= 16 readable bytes before and >= 20 after.
+// (any alignment) with aligned 16-byte stores in the body.  Threads
+// 0..nthreads-1 participate.  `src` must have >= 16 readable bytes before and
+// >= 20 after.
 __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
-                                         unsigned len) {
+                                         unsigned len, unsigned nthreads) {
   if (len == 0) return;
   const unsigned mis = (unsigned)((uintptr_t)dst & 15);  // chunk c <- src[16c - mis, +16)
   const unsigned nchunks = (mis + len + 15) >> 4;
@@ -145,7 +146,7 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   const uint32_t sbase = smem_addr(src);
   // the byte shift inside a word is the same for every chunk
   const unsigned bs = ((16u - mis) & 3u) * 8u;
-  for (unsigned c = threadIdx.x; c < nchunks; c += blockDim.x) {
+  for (unsigned c = threadIdx.x; c < nchunks; c += nthreads) {
     const int so = (int)(16 * c) - (int)mis;
     const uint32_t a = sbase + (uint32_t)((so >> 2) << 2);
     const uint32_t w0 = lds32(a), w1 = lds32(a + 4), w2 = lds32(a + 8), w3 = lds32(a + 12),
@@ -170,8 +171,26 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   }
 }
 
+// Barrier policies for the block-level collectives: the whole CTA, or a named
+// barrier over the first N threads (the compute warps of a warp-specialised CTA).
+struct SyncAll {
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+template <int ID, int N>
+struct SyncNamed {
+  __device__ __forceinline__ static void sync() {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+  }
+};
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).
-template <int THREADS>
+template <int THREADS, class Sync = SyncAll>
 __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_sums,
                                                     unsigned& total) {
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -182,7 +201,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
     if (lane >= (unsigned)o) x += y;
   }
   if (lane == 31) warp_sums[wid] = x;
-  __syncthreads();
+  Sync::sync();
   if (wid == 0) {
     unsigned t = lane < THREADS / 32 ? warp_sums[lane] : 0u;
 #pragma unroll
@@ -192,24 +211,24 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
     }
     if (lane < THREADS / 32) warp_sums[lane] = t;  // inclusive warp prefixes
   }
-  __syncthreads();
+  Sync::sync();
   total = warp_sums[THREADS / 32 - 1];
   const unsigned wbase = wid ? warp_sums[wid - 1] : 0u;
-  __syncthreads();  // warp_sums is reused by the next scan
+  Sync::sync();  // warp_sums is reused by the next scan
   return wbase + x - v;
 }
 
-template <int THREADS>
+template <int THREADS, class Sync = SyncAll>
 __device__ __forceinline__ unsigned block_min(unsigned v, unsigned* scratch) {
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
   if (lane == 0) scratch[wid] = v;
-  __syncthreads();
+  Sync::sync();
   unsigned r = scratch[0];
 #pragma unroll
   for (int i = 1; i < THREADS / 32; i++) r = min(r, scratch[i]);
-  __syncthreads();
+  Sync::sync();
   return r;
 }
 
