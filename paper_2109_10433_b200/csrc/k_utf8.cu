@@ -23,6 +23,8 @@
 //      output.
 // Tiles at the ends of the input (partial, or whose halo leaves the input)
 // and tiles containing an error take a simple masked per-character path.
+#include <cstdio>
+
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
@@ -67,6 +69,13 @@ __device__ __forceinline__ bool decode_ok(uint32_t v) {
   return cp >= lo && cp <= 0x10FFFFu && (cp < 0xD800u || cp > 0xDFFFu);
 }
 
+// Input description passed by value to out-of-line helpers (a reference to
+// the kernel parameters would force a local-memory copy of them).
+struct Src {
+  const uint8_t* base;
+  unsigned long long head, n;
+};
+
 // A thread's 64 bytes plus the word before and the word after.
 struct Words {
   uint32_t w[K8_WPT + 2];  // w[0] = previous word, w[1..16] = own, w[17] = next
@@ -78,7 +87,7 @@ __device__ __forceinline__ unsigned byte_at(const Words& W, int p) {  // p in [-
 }
 
 // Byte-granular masked load of a thread's window (ends of the input only).
-__device__ __noinline__ void load_masked(const U8Args& a, long long v0, Words& W) {
+__device__ __noinline__ void load_masked(Src a, long long v0, Words& W) {
   const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
   for (int k = 0; k < K8_WPT + 2; k++) {
     uint32_t x = 0;
@@ -93,7 +102,7 @@ __device__ __noinline__ void load_masked(const U8Args& a, long long v0, Words& W
 // Exact first error among positions [lo, hi) of the thread's bytes.  Rare
 // path: reloads the thread's window itself (byte loads), so the hot path keeps
 // its words in registers.
-__device__ __noinline__ unsigned first_error_rule_a(const U8Args& a, long long v0, unsigned lo,
+__device__ __noinline__ unsigned first_error_rule_a(Src a, long long v0, unsigned lo,
                                                     unsigned hi) {
   Words W;
   load_masked(a, v0, W);
@@ -208,7 +217,7 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
 // ---- generic path (ends of the input, tiles with an error): rare, per byte --
 // Counts (units or characters) of the characters starting at positions
 // [lo, lim) of the thread's bytes; with `dst`, also writes their units.
-__device__ __noinline__ unsigned generic_chars(const U8Args& a, long long v0, unsigned lo,
+__device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
                                                unsigned lim, bool units, uint16_t* dst) {
   Words W;
   load_masked(a, v0, W);
@@ -269,17 +278,17 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
   const uint32_t c2 = c << 1;
-  const uint32_t ascii7 = ~c & H;                 // lanes < 0x80
-  const uint32_t lead7 = ~(c & ~c2) & H;          // lanes that start a character
-  const uint32_t ge_e0 = c & c2 & (c << 2) & H;   // 3-byte (or 4-byte) leads
-  const uint32_t m1 = (ascii7 >> 7) * 0xFFu;
-  const uint32_t m3 = (ge_e0 >> 7) * 0xFFu;
-  const uint32_t A = (n1 & m3) | (c & ~m3);       // 3-byte: 2nd byte; 2-byte: lead
-  const uint32_t B = (n2 & m3) | (n1 & ~m3);      // last byte of the character
+  const uint32_t lead7 = ~(c & ~c2) & H;               // lanes that start a character
+  const uint32_t ge_e0 = c & c2 & (c << 2);            // bit 7: 3-byte (or 4-byte) lead
+  // full-byte lane masks from bit 7 (PRMT sign-replicate selectors 8..B)
+  const uint32_t mna = prmt(c, 0, 0xBA98);             // non-ASCII lanes
+  const uint32_t m3 = prmt(ge_e0, 0, 0xBA98);
+  const uint32_t A = (n1 & m3) | (c & ~m3);            // 3-byte: 2nd byte; 2-byte: lead
+  const uint32_t B = (n2 & m3) | (n1 & ~m3);           // last byte of the character
   const uint32_t lom = ((A << 6) & 0xC0C0C0C0u) | (B & 0x3F3F3F3Fu);
-  const uint32_t lo = (c & m1) | (lom & ~m1);
+  const uint32_t lo = (c & ~mna) | (lom & mna);
   const uint32_t him = ((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3);
-  const uint32_t hi = him & ~m1;
+  const uint32_t hi = him & mna;
   uint32_t u01 = prmt(lo, hi, 0x5140), u23 = prmt(lo, hi, 0x7362);
   if (!kFour) {
     if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
@@ -289,8 +298,8 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   } else {
     // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10), low = 0xDC00 | (cp & 0x3FF)
     const uint32_t n3 = prmt(c, n, 0x6543);
-    const uint32_t four7 = ge_e0 & (c << 3);
-    const uint32_t m4 = (four7 >> 7) * 0xFFu;
+    const uint32_t four7 = ge_e0 & (c << 3) & H;
+    const uint32_t m4 = prmt(four7, 0, 0xBA98);
     const uint32_t X = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
     const uint32_t c7 = c & 0x07070707u;
     const uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
@@ -324,10 +333,12 @@ struct TileCount {
 
 template <bool kTranscode, int NT, class Sync>
 __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsigned* red,
-                                           unsigned& tile_err, TileCount& tc) {
+                                           unsigned* scan, TileCount& tc, unsigned& off,
+                                           unsigned& agg) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K8_TILE;  // virtual start of the tile
   tc.v0 = vt0 + (long long)K8_BPT * threadIdx.x;
+  const Src src{a.base, a.head, a.n};
   // interior: the tile and both halo words lie inside the input
   const bool interior =
       vt0 - 4 >= (long long)a.head && vt0 + K8_TILE + 4 <= (long long)(a.head + a.n);
@@ -347,7 +358,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     tc.W.w[K8_WPT + 1] = nw;
   } else {
     Words L;
-    load_masked(a, tc.v0, L);
+    load_masked(src, tc.v0, L);
 #pragma unroll
     for (int k = 0; k < K8_WPT + 2; k++) tc.W.w[k] = L.w[k];
   }
@@ -355,26 +366,40 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
   const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
   const ClassOut co = classify(tc.W);
+  tc.four = co.four;
+  tc.lim = hi;
   unsigned my_err = kNone;
   if (co.viol || !interior || (co.susp && susp_fail(a.base + tc.v0)) ||
       (co.four && four_fail(a.base + tc.v0))) {
-    const unsigned er = first_error_rule_a(a, tc.v0, tc.lo, hi);
+    const unsigned er = first_error_rule_a(src, tc.v0, tc.lo, hi);
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
-  tile_err = block_min<NT, Sync>(my_err, red);
-  tc.simple = interior && tile_err == kNone;
-  tc.four = co.four;
-  tc.lim = hi;
+  if (interior) {
+    // fast path: one scan; bits 23..31 count the threads that found an error
+    // (at most 256 << 23 = 2^31: no wrap; counts stay below 2^23)
+    static_assert(NT <= 256 && 2 * K8_TILE < (1 << 23), "packed scan fields");
+    tc.cnt = kTranscode ? co.units : co.chars;
+    unsigned total;
+    off = block_excl_scan<NT, Sync, false>(my_err == kNone ? tc.cnt : (1u << 23), scan, total);
+    if ((total >> 23) == 0) {
+      tc.simple = true;
+      agg = total;
+      return;
+    }
+  }
+  // ends of the input, or an error in the tile: exact, clipped counts
+  const unsigned tile_err = block_min<NT, Sync>(my_err, red);
+  tc.simple = false;
   if (tile_err != kNone) {
     const unsigned start = K8_BPT * threadIdx.x;
     tc.lim = max(tc.lo, min(hi, tile_err <= start ? 0u : tile_err - start));
+    if (threadIdx.x == 0) {
+      const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
+      atomicMin(&a.ctl->err, pos);
+    }
   }
-  tc.cnt = tc.simple ? (kTranscode ? co.units : co.chars)
-                     : generic_chars(a, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
-  if (tile_err != kNone && threadIdx.x == 0) {
-    const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
-    atomicMin(&a.ctl->err, pos);
-  }
+  tc.cnt = generic_chars(src, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
+  off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
 // ---- per-tile back half: decode into the staging buffer -----------------------
@@ -390,7 +415,7 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
       for (int k = 1; k <= K8_WPT; k++) emit_word<true>(tc.W.w[k], tc.W.w[k + 1], q);
     }
   } else {
-    generic_chars(a, tc.v0, tc.lo, tc.lim, true, stage + off);
+    generic_chars(Src{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off);
   }
 }
 
@@ -441,10 +466,8 @@ __global__ void __launch_bounds__(K8_THREADS, 4) utf8_validate_kernel(U8Args a) 
     const unsigned tile = tile_s;
     if (tile >= a.ntiles) break;
     TileCount tc;
-    unsigned tile_err;
-    count_tile<false, K8_THREADS, SyncAll>(a, tile, red, tile_err, tc);
-    unsigned total;
-    block_excl_scan<K8_THREADS>(tc.cnt, scan, total);
+    unsigned off, total;
+    count_tile<false, K8_THREADS, SyncAll>(a, tile, red, scan, tc, off, total);
     if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
   }
   finalize_if_last(a, false);
@@ -503,14 +526,16 @@ __global__ void __launch_bounds__(K8_BLOCK, 3) utf8_transcode_kernel(U8Args a) {
       const unsigned tile = sm.tile;
       if (tile >= a.ntiles) break;
       TileCount tc;
-      unsigned tile_err, agg;
-      count_tile<true, K8_THREADS, ComputeSync>(a, tile, sm.red, tile_err, tc);
-      const unsigned off = block_excl_scan<K8_THREADS, ComputeSync>(tc.cnt, sm.scan, agg);
+      unsigned off, agg;
+      count_tile<true, K8_THREADS, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
       if (j > 0) {
         // tile j-1: wait for its offset, then copy it out
         bar_sync(BAR_EXCL, K8_BLOCK);
         const unsigned long long excl = sm.excl[(j - 1) & 1];
-        if (excl != ~0ull)
+        if (a.dbg & 4) {
+          if (threadIdx.x == 0) printf("tile %u j %u excl %llu prev_agg %u\n", tile, j, excl, prev_agg);
+        }
+        if (excl != ~0ull && !(a.dbg & 2))
           copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
                    reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
       }
@@ -519,7 +544,10 @@ __global__ void __launch_bounds__(K8_BLOCK, 3) utf8_transcode_kernel(U8Args a) {
         sm.agg[j & 1] = agg;
       }
       bar_arrive(BAR_AGG, K8_BLOCK);
-      emit_tile(a, tc, sm.out[j & 1], off);
+      if (a.dbg & 4) {
+        if (threadIdx.x == 0) printf("tile %u agg %u simple0 %d\n", tile, agg, (int)tc.simple);
+      }
+      if (!(a.dbg & 1)) emit_tile(a, tc, sm.out[j & 1], off);
       if (threadIdx.x == 0) sm.tile = grab_tile(a);
       prev_agg = agg;
       j++;
@@ -527,7 +555,10 @@ __global__ void __launch_bounds__(K8_BLOCK, 3) utf8_transcode_kernel(U8Args a) {
     if (j > 0) {
       bar_sync(BAR_EXCL, K8_BLOCK);
       const unsigned long long excl = sm.excl[(j - 1) & 1];
-      if (excl != ~0ull)
+      if (a.dbg & 4) {
+        if (threadIdx.x == 0) printf("final j %u excl %llu prev_agg %u\n", j, excl, prev_agg);
+      }
+      if (excl != ~0ull && !(a.dbg & 2))
         copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
                  reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
     }

@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -145,6 +146,11 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
   a.base = reinterpret_cast<const uint8_t*>(p - a.head);
   a.n = n;
   a.ntiles = vt::tiles_utf8(a.head, n);
+  static const unsigned dbg = [] {
+    const char* e = std::getenv("VT_DEBUG");
+    return e ? (unsigned)std::strtoul(e, nullptr, 0) : 0u;
+  }();
+  a.dbg = dbg;
   VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
   a.out = d_out;
   a.status = sc->status;

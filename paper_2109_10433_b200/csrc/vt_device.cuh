@@ -136,7 +136,7 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 // Copies `len` bytes from shared memory `src` (16-byte aligned) to global `dst`
 // (any alignment) with aligned 16-byte stores in the body.  Threads
 // 0..nthreads-1 participate.  `src` must have >= 16 readable bytes before and
-// >= 20 after.
+// >= 32 after.
 __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
                                          unsigned len, unsigned nthreads) {
   if (len == 0) return;
@@ -144,13 +144,24 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   const unsigned nchunks = (mis + len + 15) >> 4;
   uint8_t* dbase = dst - mis;
   const uint32_t sbase = smem_addr(src);
-  // the byte shift inside a word is the same for every chunk
-  const unsigned bs = ((16u - mis) & 3u) * 8u;
+  // chunk c needs source bytes [16c - mis, +16): words ws..ws+4 of the two
+  // aligned 16-byte source chunks starting at 16(c-1) (+16 for mis == 0), then
+  // a byte funnel shift.  ws and the shift are the same for every chunk.
+  const unsigned rel = (16u - mis) & 15u;  // (16c - mis) mod 16
+  const unsigned ws = rel >> 2, bs = (rel & 3u) * 8u;
+  const int cbias = mis ? -1 : 0;
   for (unsigned c = threadIdx.x; c < nchunks; c += nthreads) {
-    const int so = (int)(16 * c) - (int)mis;
-    const uint32_t a = sbase + (uint32_t)((so >> 2) << 2);
-    const uint32_t w0 = lds32(a), w1 = lds32(a + 4), w2 = lds32(a + 8), w3 = lds32(a + 12),
-                   w4 = lds32(a + 16);
+    const uint32_t a = sbase + (uint32_t)(16 * ((int)c + cbias));
+    uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(a));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3) : "r"(a + 16));
+    uint32_t w0, w1, w2, w3, w4;
+    if (ws == 0) { w0 = x0; w1 = x1; w2 = x2; w3 = x3; w4 = y0; }
+    else if (ws == 1) { w0 = x1; w1 = x2; w2 = x3; w3 = y0; w4 = y1; }
+    else if (ws == 2) { w0 = x2; w1 = x3; w2 = y0; w3 = y1; w4 = y2; }
+    else { w0 = x3; w1 = y0; w2 = y1; w3 = y2; w4 = y3; }
     uint4 v;
     v.x = __funnelshift_r(w0, w1, bs);
     v.y = __funnelshift_r(w1, w2, bs);
@@ -190,7 +201,9 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).
-template <int THREADS, class Sync = SyncAll>
+// kTrailing: end with a barrier so warp_sums can be reused at once; callers
+// that pass a barrier before the next scan anyway can drop it.
+template <int THREADS, class Sync = SyncAll, bool kTrailing = true>
 __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_sums,
                                                     unsigned& total) {
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -214,7 +227,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
   Sync::sync();
   total = warp_sums[THREADS / 32 - 1];
   const unsigned wbase = wid ? warp_sums[wid - 1] : 0u;
-  Sync::sync();  // warp_sums is reused by the next scan
+  if (kTrailing) Sync::sync();  // warp_sums is reused by the next scan
   return wbase + x - v;
 }
 

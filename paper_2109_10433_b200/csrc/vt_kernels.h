@@ -24,6 +24,7 @@ struct U8Args {
   unsigned long long* status;
   Ctl* ctl;
   vt_result* res;
+  unsigned dbg;  // debug switches (VT_DEBUG env), 0 in production
 };
 
 // UTF-16 side: same conventions in units (`head` in units, 0..7).
