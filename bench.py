@@ -1,18 +1,20 @@
-"""Benchmark of the validated UTF-8 -> UTF-16LE hot path on B200.
+"""Benchmark of the validated UTF-8 <-> UTF-16LE hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
-Workload (BASELINE.json configs[1], "cfg2"): 1 GiB of valid UTF-8, CJK-heavy
-(75% U+4E00-9FFF, 20% ASCII events with runs, 5% U+0080-07FF), seeded and
-generated directly in HBM (synthetic stand-in for the paper's corpora).  A
-step is one validating transcode of the whole input through the device-pointer
-C ABI (vt_utf8_to_utf16_async) -- one kernel launch.  The input (1 GiB) is
-larger than the 126 MB L2, so no flush is needed between steps.
+Default workload (BASELINE.json configs[1], "cfg2"): 1 GiB of valid UTF-8,
+CJK-heavy (75% U+4E00-9FFF, 20% ASCII events with runs, 5% U+0080-07FF),
+seeded and generated directly in HBM (synthetic stand-in for the paper's
+corpora).  A step is one validating UTF-8 -> UTF-16LE transcode of the whole
+input through the device-pointer C ABI (vt_utf8_to_utf16_async): one kernel
+launch.  The 1 GiB input is larger than the 126 MB L2, so no flush is needed
+between steps.  Other configs can be measured with --config (1, 3, 4, 5; 3 is
+UTF-16LE -> UTF-8, 5 the 4 GiB round trip UTF-8 -> UTF-16 -> UTF-8).
 
 Metric: input GB/s (aggregate over GPUs) with Gchar/s and the HBM roofline
-fraction beside it.  Multi-GPU (torchrun, one process per GPU): weak scaling,
-each rank transcodes its own 1 GiB slice of the stream (disjoint chunk ranges);
-no data-path collective, timing is the max over ranks.
+fraction of the kernel beside it.  Multi-GPU (torchrun, one process per GPU):
+weak scaling, each rank transcodes its own slice of the stream (disjoint chunk
+ranges); no data-path collective, timing is the max over ranks.
 
 ``--impl reference`` times the reference's own CPU implementation (the
 unmodified library compiled out of tree into oracle/_ref, SIMD path, on
@@ -32,12 +34,15 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# cfg: (description, input elements (bytes; units for cfg 3), direction)
 CONFIGS = {
-    1: ("cfg1: UTF-8->UTF-16LE validating, 16 MiB, 90% U+0020-007E / 10% U+0080-07FF", 16 << 20, "utf8"),
+    1: ("cfg1: UTF-8->UTF-16LE validating, 16 MiB, 90% U+0020-007E / 10% U+0080-07FF", 16 << 20, "u8"),
     2: ("cfg2: UTF-8->UTF-16LE validating, 1 GiB, 75% U+4E00-9FFF / 20% ASCII (runs) / 5% U+0080-07FF",
-        1 << 30, "utf8"),
-    3: ("cfg3: UTF-16LE->UTF-8, 1 GiB UTF-16, 60/15/15/10% 1/2/3/4-byte classes", 1 << 29, "utf16"),
-    4: ("cfg4: UTF-8->UTF-16LE validating, 1 GiB, 25/25/25/25% + ~1 error per 64 MiB", 1 << 30, "utf8"),
+        1 << 30, "u8"),
+    3: ("cfg3: UTF-16LE->UTF-8, 1 GiB of UTF-16 (2^29 units), 60/15/15/10% 1/2/3/4-byte classes", 1 << 29,
+        "u16"),
+    4: ("cfg4: UTF-8->UTF-16LE validating, 1 GiB, 25/25/25/25% + ~1 error per 64 MiB", 1 << 30, "u8"),
+    5: ("cfg5: round trip UTF-8->UTF-16LE->UTF-8, 4 GiB per GPU, cfg-3 mix", 4 << 30, "rt"),
 }
 
 
@@ -101,90 +106,99 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(busy)}
 
 
-def cpu_baseline_run(host_in, threads: int, reps: int, kind_pref: str = "reference"):
-    """Times the reference CPU path (oracle/_ref, all host threads) -- or the
-    oracle port when the reference build is missing -- on host_in."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
+def _char_boundary(host, m, kind):
+    """Largest whole-character prefix length <= m."""
+    if kind == "u16":
+        if m < len(host) and 0xDC00 <= int(host[m]) <= 0xDFFF:
+            m -= 1
+        return m
+    while 0 < m < len(host) and (host[m] & 0xC0) == 0x80:
+        m -= 1
+    return m
+
+
+def cpu_reference_runner(kind):
+    """The reference CPU path (oracle/_ref, SIMD, sharded) or, if that build is
+    missing, the oracle port.  Returns (run(host, threads) -> result, kind)."""
     import numpy as np
 
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import Oracle, Reference
 
     if Reference.available():
-        ref, kind = Reference(), "reference"
-        run = lambda: ref.utf8_to_utf16(host_in, threads=threads, out=out)
+        impl, ck = Reference(), "reference"
     else:
-        orc, kind = Oracle(), "port"
-        run = lambda: orc.utf8_to_utf16(host_in, threads=threads)
-    out = np.empty(len(host_in) + 8, dtype=np.uint16)
-    best = None
-    res = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        _, res = run()
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return best, kind, res
+        impl, ck = Oracle(), "port"
+    bufs = {}
+
+    def run(host, threads):
+        if kind == "u16":
+            out = bufs.get(len(host))
+            if out is None and ck == "reference":
+                out = bufs[len(host)] = np.empty(3 * len(host) + 16, dtype=np.uint8)
+            if ck == "reference":
+                return impl.utf16_to_utf8(host, threads=threads, out=out)[1]
+            return impl.utf16_to_utf8(host, threads=threads)[1]
+        out = bufs.get(len(host))
+        if out is None and ck == "reference":
+            out = bufs[len(host)] = np.empty(len(host) + 8, dtype=np.uint16)
+        if ck == "reference":
+            return impl.utf8_to_utf16(host, threads=threads, out=out)[1]
+        return impl.utf8_to_utf16(host, threads=threads)[1]
+
+    return run, ck
 
 
-def run_reference_arm(args, rank: int):
-    """--impl reference: the reference's own CPU implementation on this box."""
+def host_input(cfg, size):
+    """The workload generated on the host (same generator as the device one)."""
     import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
     import paper_2109_10433_b200 as vt
 
-    if rank != 0:
-        return None
-    desc, size, kind = CONFIGS[args.config]
-    # input on the host via the host-side generator (no GPU involved)
-    draws = int(vt.lib().vt_gen_chunk_draws(args.config))
-    chunks = []
-    total = 0
-    c = 0
-    from concurrent.futures import ThreadPoolExecutor
-
+    chunks, total, c = [], 0, 0
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         while total < size:
-            batch = list(ex.map(lambda k: vt.generate_host_chunk(args.config, args.config, k)[0],
-                                range(c, c + 256)))
-            c += 256
-            for a in batch:
+            for a in ex.map(lambda k: vt.generate_host_chunk(cfg, cfg, k)[0], range(c, c + 256)):
                 chunks.append(a)
                 total += len(a)
                 if total >= size:
                     break
+            c += 256
     host = np.concatenate(chunks)
-    n = size
-    while n > 0 and (host[n] & 0xC0) == 0x80:
-        n -= 1  # cut at a character boundary
-    host = np.ascontiguousarray(host[:n])
-    threads = os.cpu_count() or 1
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import Oracle, Reference
+    n = _char_boundary(host, size, "u16" if cfg == 3 else "u8")
+    return np.ascontiguousarray(host[:n])
 
-    out = np.empty(n + 8, dtype=np.uint16)
-    if Reference.available():
-        impl, ck = Reference(), "reference"
-        step = lambda: impl.utf8_to_utf16(host, threads=threads, out=out)
-    else:
-        impl, ck = Oracle(), "port"
-        step = lambda: impl.utf8_to_utf16(host, threads=threads)
+
+def run_reference_arm(args, rank):
+    """--impl reference: the reference's own CPU implementation on this box."""
+    if rank != 0:
+        return None
+    desc, size, kind = CONFIGS[args.config]
+    if kind == "rt":
+        kind, size = "u8", 1 << 30  # the CPU round trip is timed on its first leg, 1 GiB
+    host = host_input(3 if kind == "u16" else args.config if args.config != 5 else 5, size)
+    threads = os.cpu_count() or 1
+    run, ck = cpu_reference_runner(kind)
     for _ in range(args.warmup):
-        step()
+        run(host, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, r = step()
+        r = run(host, threads)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
-    gbs = n / t / 1e9
+    in_bytes = host.nbytes
+    gbs = in_bytes / t / 1e9
     return {
-        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)", "value": round(gbs, 4), "unit": "GB/s",
-        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded generator, BASELINE cfg2 shape)",
-        "config": {"workload": desc, "input_bytes": n, "parallelism": f"cpu x{threads} threads"},
+        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)" if kind == "u8" else "input GB/s (UTF-16LE -> UTF-8)",
+        "value": round(gbs, 4), "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": f"synthetic (seeded generator, BASELINE cfg{args.config} shape)",
+        "config": {"workload": desc, "input_bytes": in_bytes, "parallelism": f"cpu x{threads} threads"},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": ck,
-                         "sample": f"whole cfg{args.config} input ({n} bytes) per step, "
+                         "sample": f"whole cfg{args.config} input ({in_bytes} bytes) per step, "
                                    f"reference SIMD path on {threads} character-boundary shards"},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result": {"consumed": r.consumed, "written": r.written, "error_at": r.error_at},
@@ -197,7 +211,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -225,22 +239,44 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     desc, size, kind = CONFIGS[args.config]
+    gen_cfg = args.config
     # each rank its own slice of the stream: disjoint chunk ranges
-    d_in, n, first_bad = vt.generate(args.config, size, chunk0=rank * 1_000_000)
+    d_in, n, first_bad = vt.generate(gen_cfg, size, chunk0=rank * 1_000_000)
     torch.cuda.synchronize()
-    d_out = torch.empty(n + 8, dtype=torch.int16, device="cuda")
-    d_res = torch.zeros(3, dtype=torch.int64, device="cuda")
     stream = torch.cuda.current_stream()
+    d_res = torch.zeros(3, dtype=torch.int64, device="cuda")
+    d_res2 = torch.zeros(3, dtype=torch.int64, device="cuda")
+    if kind == "u16":
+        d_out = torch.empty(3 * n + 16, dtype=torch.uint8, device="cuda")
+        in_bytes = 2 * n
 
-    def step():
-        vt.utf8_to_utf16_device(d_in, n, d_out, stream=stream, d_res=d_res)
+        def step():
+            vt.utf16_to_utf8_device(d_in, n, d_out, stream=stream, d_res=d_res)
+        kernel = "vt::utf16_transcode_kernel"
+    elif kind == "u8":
+        d_out = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+        in_bytes = n
+
+        def step():
+            vt.utf8_to_utf16_device(d_in, n, d_out, stream=stream, d_res=d_res)
+        kernel = "vt::utf8_transcode_kernel"
+    else:  # round trip: the UTF-16 length is known from one warm-up pass
+        d16 = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+        r16 = vt.utf8_to_utf16_device(d_in, n, d16)
+        n16 = r16.written
+        d_out = torch.empty(3 * n16 + 16, dtype=torch.uint8, device="cuda")
+        in_bytes = n
+
+        def step():
+            vt.utf8_to_utf16_device(d_in, n, d16, stream=stream, d_res=d_res)
+            vt.utf16_to_utf8_device(d16, n16, d_out, stream=stream, d_res=d_res2)
+        kernel = "vt::utf8_transcode_kernel + vt::utf16_transcode_kernel"
 
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
-        # keep the GPU busy long enough for nvidia-smi to see the load
-        t_end = time.time() + 0.6
+        t_end = time.time() + 0.6  # keep the GPU busy long enough for nvidia-smi to see it
         while time.time() < t_end:
             step()
             torch.cuda.synchronize()
@@ -259,6 +295,10 @@ def main():
             dist.barrier()
         ms = e0.elapsed_time(e1)
     res = vt.result_from_device(d_res)
+    if kind == "rt":
+        res2 = vt.result_from_device(d_res2)
+        assert res2.error_at is None and res2.written == n and torch.equal(d_out[:n], d_in[:n]), \
+            "round trip did not reproduce the input"
     ms_max = ms
     if dist:
         t = torch.tensor([ms], device="cuda")
@@ -271,29 +311,39 @@ def main():
                             device="cuda")
         allr = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(world)]
         dist.all_gather(allr, mine)
-        ns = torch.tensor([n], device="cuda")
         alln = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
-        dist.all_gather(alln, ns)
+        dist.all_gather(alln, torch.tensor([n], device="cuda"))
         starts = np.concatenate([[0], np.cumsum([int(x.item()) for x in alln])]).tolist()
         rs = [TranscodeResult(int(x[0]), int(x[1]), None if int(x[2]) < 0 else int(x[2])) for x in allr]
-        total_n = starts[-1]
-        gres, _ = sharding.combine(starts, rs, total_n)
+        gres, _ = sharding.combine(starts, rs, starts[-1])
+        tot = torch.tensor([in_bytes], device="cuda")
+        dist.all_reduce(tot)
+        total_in = int(tot.item())
     else:
-        total_n = n
         gres = res
+        total_in = in_bytes
     per_step_ms = ms_max / args.steps
-    chars = vt.validate_utf8_device(d_in, n).written  # code points of this rank's slice
+    if kind == "u16":
+        chars = vt.validate_utf16_device(d_in, n).written
+        alg_bytes = 2 * n + res.written
+    elif kind == "u8":
+        chars = vt.validate_utf8_device(d_in, n).written
+        alg_bytes = n + 2 * res.written
+    else:
+        chars = vt.validate_utf8_device(d_in, n).written
+        alg_bytes = 2 * n + 4 * res.written  # 8->16 (n + 2 u16) + 16->8 (2 u16 + n)
     if dist:
         c = torch.tensor([chars], device="cuda")
         dist.all_reduce(c)
         chars = int(c.item())
-    value = total_n / (per_step_ms / 1e3) / 1e9
+    value = total_in / (per_step_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
-    alg_bytes = n + 2 * res.written  # per launch, this rank
     achieved = alg_bytes / (ms / args.steps / 1e3) / 1e9
-
+    metric = ("input GB/s (UTF-16LE -> UTF-8)" if kind == "u16" else
+              "input GB/s (validated UTF-8 -> UTF-16LE)" if kind == "u8" else
+              "input GB/s (UTF-8 -> UTF-16LE -> UTF-8 round trip)")
     line = {
-        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)",
+        "metric": metric,
         "value": round(value, 2),
         "unit": "GB/s",
         "n_gpus": world,
@@ -303,16 +353,17 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u8",
+        "dtype": "u16" if kind == "u16" else "u8",
         "data": "synthetic (seeded splitmix64 chunk generator in HBM, BASELINE cfg shape; corpora absent)",
-        "config": {"workload": desc, "input_bytes_per_gpu": n, "output_units_per_gpu": res.written,
-                   "chars_total": chars, "l2": "input 1 GiB > 126 MB L2: no flush between steps",
+        "config": {"workload": desc, "input_bytes_per_gpu": in_bytes, "output_elems_per_gpu": res.written,
+                   "chars_total": chars,
+                   "l2": ("input > 126 MB L2: no flush between steps" if in_bytes > (256 << 20)
+                          else "input fits L2: steps re-read it from L2 (cfg1 is launch-latency bound)"),
                    "parallelism": f"shards x{world} (no collective)" if world > 1 else "single GPU"},
         "gchars_per_s": round(chars / (per_step_ms / 1e3) / 1e9, 2),
         "result": {"consumed": gres.consumed, "written": gres.written, "error_at": gres.error_at},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": "vt::utf8_kernel<true>",
+                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": kernel,
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
@@ -325,20 +376,27 @@ def main():
             line["roofline"]["traffic"] = t["dram_bytes_per_launch"]
             line["roofline"]["traffic_source"] = t["source"]
 
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if rank == 0 and world == 1 and not args.no_e2e and kind != "rt":
         # end to end through the drop-in (host-pointer) C ABI: pinned host input,
         # H2D + kernel + D2H of result and output inside the timed region
-        h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        h_in.copy_(d_in[:n])
-        h_out = torch.empty(n + 8, dtype=torch.int16, pin_memory=True)
         import ctypes
 
         L = vt.lib()
         r = vt._CRes()
+        if kind == "u8":
+            h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            h_in.copy_(d_in[:n])
+            h_out = torch.empty(n + 8, dtype=torch.int16, pin_memory=True)
+            fn, elem_out = L.vt_host_utf8_to_utf16, 2
+        else:
+            h_in = torch.empty(n, dtype=torch.int16, pin_memory=True)
+            h_in.copy_(d_in[:n])
+            h_out = torch.empty(3 * n + 16, dtype=torch.uint8, pin_memory=True)
+            fn, elem_out = L.vt_host_utf16_to_utf8, 1
 
         def e2e_step():
-            rc = L.vt_host_utf8_to_utf16(h_in.data_ptr(), n, h_out.data_ptr(), ctypes.byref(r))
-            assert rc == 0
+            rc = fn(h_in.data_ptr(), n, h_out.data_ptr(), ctypes.byref(r))
+            assert rc == 0, rc
         for _ in range(2):
             e2e_step()
         k = max(3, min(args.steps, 10))
@@ -347,27 +405,38 @@ def main():
             e2e_step()
         dt = (time.perf_counter() - t0) / k
         assert r.written == res.written and r.error_at == (-1 if res.error_at is None else res.error_at)
-        line["e2e"] = {"value": round(n / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n,
-                       "d2h_bytes_per_step": 2 * int(r.written) + 24,
-                       "api": "vt_host_utf8_to_utf16 (drop-in boundary), pinned host buffers",
+        line["e2e"] = {"value": round(in_bytes / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": in_bytes,
+                       "d2h_bytes_per_step": elem_out * int(r.written) + 24,
+                       "api": f"{fn.__name__} (drop-in boundary), pinned host buffers",
                        "ms_per_step": round(dt * 1e3, 3)}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ckind = "u16" if kind == "u16" else "u8"
         host = d_in[:n].cpu().numpy()
+        if ckind == "u16":
+            host = host.view(np.uint16)
         threads = os.cpu_count() or 1
-        t, kind_, cres = cpu_baseline_run(host, threads, reps=3)
-        assert cres.written == res.written and cres.error_at == res.error_at, "CPU baseline disagrees"
+        run, ck = cpu_reference_runner(ckind)
+        best, cres = None, None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            cres = run(host, threads)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        if kind != "rt":
+            assert cres.written == res.written and cres.error_at == res.error_at, "CPU baseline disagrees"
         # the reference's own design point: one thread, on a 64 MiB prefix
-        m = 64 << 20
-        while m > 0 and (host[m] & 0xC0) == 0x80:
-            m -= 1
-        t1, _, _ = cpu_baseline_run(host[:m], 1, reps=2)
+        m = _char_boundary(host, (64 << 20) // host.itemsize, ckind)
+        t0 = time.perf_counter()
+        run(host[:m], 1)
+        t1 = time.perf_counter() - t0
         line["cpu_baseline"] = {
-            "value": round(n / t / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind_,
-            "sample": f"whole cfg{args.config} input ({n} bytes), reference SIMD path (oracle/_ref, "
-                      f"-O3 SSE4.1) on {threads} character-boundary shards, best of 3; "
-                      f"1-thread on a {m}-byte prefix: {m / t1 / 1e9:.3f} GB/s",
-            "single_thread_gbs": round(m / t1 / 1e9, 3),
+            "value": round(host.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": ck,
+            "sample": f"whole cfg{args.config} input ({host.nbytes} bytes{', first leg' if kind == 'rt' else ''}), "
+                      f"reference SIMD path (oracle/_ref, -O3 SSE4.1) on {threads} character-boundary "
+                      f"shards, best of 3; 1 thread on a {m * host.itemsize}-byte prefix: "
+                      f"{m * host.itemsize / t1 / 1e9:.3f} GB/s",
+            "single_thread_gbs": round(m * host.itemsize / t1 / 1e9, 3),
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -3,249 +3,331 @@
 //
 // Replaces the reference's 8-unit register dispatch with its pack tables and
 // scalar surrogate fallback (proj/src/utf16_to_utf8.cpp:12-107) and the
-// surrogate scan of proj/src/validation.cpp:51-77.  The GPU needs no tables:
-// every unit's UTF-8 length is a function of the unit and its neighbours
-// (<0x80: 1, <0x800: 2, high surrogate followed by low: 4, the low: 0, other
-// BMP: 3) and the first error is the first unit failing the local pairing rule
-// (SURVEY.md 8(a) fact C), which is exactly where the scalar decoder
-// (proj/src/codec_core.cpp:74-83,106-125) stops.  Same tile pipeline as
-// k_utf8.cu: smem staging with a one-unit halo, per-thread lengths, block scan,
-// decoupled look-back, encode into smem, aligned 16-byte stores.
-#include "vt_device.cuh"
+// surrogate scan of proj/src/validation.cpp:51-77.  No tables: a unit's UTF-8
+// length is a function of the unit and its neighbours (<0x80: 1, <0x800: 2,
+// high surrogate followed by a low one: 4, that low one: 0, other BMP: 3), and
+// the first error is the first unit failing the local pairing rule (SURVEY.md
+// 8(a) fact C) -- exactly where the scalar decoder (proj/src/codec_core.cpp:
+// 74-83,106-125) stops.
+//
+// Same tile pipeline as k_utf8.cu (vt_pipeline.cuh).  Per 8192-unit tile each
+// thread owns 32 consecutive units (16 words of two units):
+//   A. SWAR over 16-bit lanes: high/low-surrogate planes, the pairing check
+//      against the neighbouring units, and the byte count (lengths summed
+//      in 16-bit lane counters);
+//   B. a thread that sees an error finds its exact first failing unit; tiles
+//      with an error, and the tiles at the ends of the input, take a masked
+//      per-unit path;
+//   C. encode: per unit the UTF-8 bytes are assembled in one register
+//      (bit fields spread by shifts, lead marks or'ed in) and stored byte-wise
+//      into the shared-memory staging buffer.
 #include "vt_kernels.h"
+#include "vt_pipeline.cuh"
 
 namespace vt {
 
-constexpr int U16_THREADS = 256;
-constexpr int U16_ROWS = 2;
-constexpr int U16_ROW = U16_THREADS * 8;      // units per row
-constexpr int U16_TILE = U16_ROW * U16_ROWS;  // units per tile
+constexpr int K16_WPT = 16;                              // words (2 units) per thread
+constexpr int K16_UPT = 2 * K16_WPT;                     // units per thread
+constexpr int K16_TILE = kComputeThreads * K16_UPT;      // units per tile
 constexpr unsigned kNone16 = 0xFFFFFFFFu;
+constexpr uint32_t H16 = 0x80008000u;
 
-struct U16Smem {
-  alignas(16) uint16_t in[8 + U16_TILE + 8];
-  alignas(16) uint8_t out_pad[32];
-  alignas(16) uint8_t out[3 * U16_TILE];
-  alignas(16) uint8_t out_tail[32];
-  unsigned scan[U16_THREADS / 32];
-  unsigned red[U16_THREADS / 32];
-  unsigned long long excl;
-  unsigned tile;
+// bit 15 of each 16-bit lane: v != 0, for v with bits only in 10..15 / 26..31
+__device__ __forceinline__ uint32_t nz_hi6(uint32_t v) {
+  return ((v >> 1) + 0x7E007E00u) & H16;
+}
+
+struct Src16 {
+  const uint16_t* base;
+  unsigned long long head, n;
 };
+
+struct Words16 {
+  uint32_t w[K16_WPT + 2];  // w[0] = previous word, w[1..16] own, w[17] next
+};
+
+__device__ __forceinline__ unsigned unit_at(const Words16& W, int i) {  // i in [-2, 34)
+  const int q = i + 2;
+  return (W.w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
+}
+
+__device__ __noinline__ void load_masked16(Src16 a, long long v0, Words16& W) {
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  for (int k = 0; k < K16_WPT + 2; k++) {
+    uint32_t x = 0;
+    for (int b = 0; b < 2; b++) {
+      const long long p = v0 - 2 + 2 * k + b;
+      if (p >= lo && p < hi) x |= (uint32_t)a.base[p] << (16 * b);
+    }
+    W.w[k] = x;
+  }
+}
 
 __device__ __forceinline__ bool is_hi(unsigned u) { return (u & 0xFC00u) == 0xD800u; }
 __device__ __forceinline__ bool is_lo(unsigned u) { return (u & 0xFC00u) == 0xDC00u; }
 
-__device__ __forceinline__ void load_tile16(const U16Args& a, unsigned tile, uint16_t* in_s) {
-  // virtual unit v lives at in_s[8 + v - tile*U16_TILE]; chunks are 8 units
-  const unsigned long long vbase = (unsigned long long)tile * U16_TILE;
-  const unsigned long long vend = a.head + a.n;
-  for (int j = threadIdx.x; j < U16_TILE / 8 + 2; j += U16_THREADS) {
-    const long long vc = (long long)vbase - 8 + 8LL * j;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (vc >= 0 && (unsigned long long)vc < vend && (unsigned long long)vc + 8 > a.head) {
-      v = __ldcs(reinterpret_cast<const uint4*>(a.base + vc));
-      if ((unsigned long long)vc < a.head || (unsigned long long)vc + 8 > vend) {
-        uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const unsigned long long pos = (unsigned long long)vc + u;
-          if (pos < a.head || pos >= vend) w[u >> 1] &= (u & 1) ? 0x0000FFFFu : 0xFFFF0000u;
-        }
-        v = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-    }
-    *reinterpret_cast<uint4*>(in_s + 8 * j) = v;
+// UTF-8 bytes of the unit at position i (little-endian in the result) and
+// their number; `nx` is the unit after it.
+__device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned nx, unsigned& len) {
+  unsigned cp = u;
+  if (u < 0x80u) {
+    len = 1;
+    return u;
   }
-}
-
-struct Row16 {
-  unsigned u[8];
-  unsigned prev, next;
-  unsigned lo, hi;  // in-input unit positions [lo, hi)
-};
-
-__device__ __forceinline__ unsigned utf8_len(const Row16& r, int i) {
-  const unsigned u = r.u[i];
-  if (u < 0x80u) return 1;
-  if (u < 0x800u) return 2;
-  if (is_hi(u)) return 4;
-  if (is_lo(u)) return 0;
-  return 3;
-}
-
-__device__ __forceinline__ unsigned first_error16(const Row16& r) {
-  unsigned e = kNone16;
-#pragma unroll
-  for (int i = 7; i >= 0; i--) {
-    const unsigned u = r.u[i];
-    const unsigned p = i ? r.u[i - 1] : r.prev;
-    const unsigned q = i < 7 ? r.u[i + 1] : r.next;
-    const bool bad = (is_lo(u) && !is_hi(p)) || (is_hi(u) && !is_lo(q));
-    if (bad && (unsigned)i >= r.lo && (unsigned)i < r.hi) e = i;
+  if (u < 0x800u) {
+    len = 2;
+    return 0x80C0u | (u >> 6) | ((u & 0x3Fu) << 8);
   }
-  return e;
+  if (is_lo(u)) {
+    len = 0;
+    return 0;
+  }
+  if (is_hi(u)) {
+    cp = 0x10000u + (((u & 0x3FFu) << 10) | (nx & 0x3FFu));
+    len = 4;
+    return 0x808080F0u | (cp >> 18) | (((cp >> 12) & 0x3Fu) << 8) | (((cp >> 6) & 0x3Fu) << 16) |
+           ((cp & 0x3Fu) << 24);
+  }
+  len = 3;
+  return 0x8080E0u | (u >> 12) | (((u >> 6) & 0x3Fu) << 8) | ((u & 0x3Fu) << 16);
 }
 
-template <bool kTranscode>
-__global__ void __launch_bounds__(U16_THREADS) utf16_kernel(U16Args a) {
-  __shared__ U16Smem sm;
-  while (true) {
-    if (threadIdx.x == 0) {
-      unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
-      const unsigned long long e = load_relaxed(&a.ctl->err);
-      if (t < a.ntiles && e != kNoError && (e + a.head) / U16_TILE < t) t = a.ntiles;
-      sm.tile = t;
-    }
-    __syncthreads();
-    const unsigned tile = sm.tile;
-    if (tile >= a.ntiles) break;
-    load_tile16(a, tile, sm.in);
-    __syncthreads();
+// Masked per-unit path (ends of the input, tiles with an error): exact first
+// error among [lo, hi), or with `count`: bytes / code points of [lo, lim).
+__device__ __noinline__ unsigned first_error16(Src16 a, long long v0, unsigned lo, unsigned hi) {
+  Words16 W;
+  load_masked16(a, v0, W);
+  for (unsigned i = lo; i < hi; i++) {
+    const unsigned u = unit_at(W, (int)i);
+    if (is_lo(u) && !is_hi(unit_at(W, (int)i - 1))) return i;
+    if (is_hi(u) && !is_lo(unit_at(W, (int)i + 1))) return i;
+  }
+  return kNone16;
+}
 
-    Row16 row[U16_ROWS];
-    unsigned my_err = kNone16;
-#pragma unroll
-    for (int r = 0; r < U16_ROWS; r++) {
-      const uint16_t* p = sm.in + 8 + r * U16_ROW + 8 * threadIdx.x;
-      const uint4 v = *reinterpret_cast<const uint4*>(p);
-      row[r].u[0] = v.x & 0xFFFF; row[r].u[1] = v.x >> 16;
-      row[r].u[2] = v.y & 0xFFFF; row[r].u[3] = v.y >> 16;
-      row[r].u[4] = v.z & 0xFFFF; row[r].u[5] = v.z >> 16;
-      row[r].u[6] = v.w & 0xFFFF; row[r].u[7] = v.w >> 16;
-      row[r].prev = p[-1];
-      row[r].next = p[8];
-      const long long v0 = (long long)tile * U16_TILE + r * U16_ROW + 8 * threadIdx.x;
-      const long long s = (long long)a.head - v0, e = (long long)(a.head + a.n) - v0;
-      row[r].lo = (unsigned)max(0LL, min(8LL, s));
-      row[r].hi = (unsigned)max((long long)row[r].lo, min(8LL, e));
-      const unsigned er = first_error16(row[r]);
-      if (er != kNone16 && my_err == kNone16) my_err = r * U16_ROW + 8 * threadIdx.x + er;
-    }
-    const unsigned tile_err = block_min<U16_THREADS>(my_err, sm.red);
-    unsigned cnt[U16_ROWS];
-#pragma unroll
-    for (int r = 0; r < U16_ROWS; r++) {
-      const unsigned start = r * U16_ROW + 8 * threadIdx.x;
-      unsigned lim = row[r].hi;
-      if (tile_err != kNone16) lim = min(lim, tile_err <= start ? 0u : tile_err - start);
-      row[r].hi = max(lim, row[r].lo);
-      unsigned c = 0;
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        if ((unsigned)i >= row[r].lo && (unsigned)i < row[r].hi)
-          c += kTranscode ? utf8_len(row[r], i) : (is_lo(row[r].u[i]) ? 0u : 1u);
-      }
-      cnt[r] = c;
-    }
-    if (tile_err != kNone16 && threadIdx.x == 0) {
-      const unsigned long long pos = (unsigned long long)tile * U16_TILE + tile_err - a.head;
-      atomicMin(&a.ctl->err, pos);
-    }
-    if (!kTranscode) {
-      unsigned total;
-      block_excl_scan<U16_THREADS>(cnt[0] + cnt[1], sm.scan, total);
-      if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
-      __syncthreads();
+__device__ __noinline__ unsigned generic_units(Src16 a, long long v0, unsigned lo, unsigned lim,
+                                               bool bytes, uint8_t* dst) {
+  Words16 W;
+  load_masked16(a, v0, W);
+  unsigned q = 0;
+  for (unsigned i = lo; i < lim; i++) {
+    const unsigned u = unit_at(W, (int)i);
+    unsigned len;
+    const uint32_t p = encode_unit(u, unit_at(W, (int)i + 1), len);
+    if (!bytes) {
+      q += is_lo(u) ? 0u : 1u;
       continue;
     }
-    unsigned tot0, tot1;
-    const unsigned off0 = block_excl_scan<U16_THREADS>(cnt[0], sm.scan, tot0);
-    const unsigned off1 = block_excl_scan<U16_THREADS>(cnt[1], sm.scan, tot1) + tot0;
-    const unsigned agg = tot0 + tot1;
-    if (threadIdx.x < 32) {
-      unsigned long long excl = 0;
-      if (tile == 0) {
-        if (threadIdx.x == 0) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
-      } else {
-        if (threadIdx.x == 0) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
-        excl = lookback(a.status, a.epoch, tile, a.ctl, U16_TILE, a.head);
-        if (threadIdx.x == 0 && excl != ~0ull)
-          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
-      }
-      if (threadIdx.x == 0) sm.excl = excl;
-    }
-#pragma unroll
-    for (int r = 0; r < U16_ROWS; r++) {
-      uint8_t* d = sm.out + (r ? off1 : off0);
-      unsigned q = 0;
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        if ((unsigned)i < row[r].lo || (unsigned)i >= row[r].hi) continue;
-        const unsigned u = row[r].u[i];
-        if (u < 0x80u) {
-          d[q++] = (uint8_t)u;
-        } else if (u < 0x800u) {
-          d[q] = (uint8_t)(0xC0u | (u >> 6));
-          d[q + 1] = (uint8_t)(0x80u | (u & 0x3Fu));
-          q += 2;
-        } else if (is_hi(u)) {
-          const unsigned nx = i < 7 ? row[r].u[i + 1] : row[r].next;
-          const unsigned cp = 0x10000u + (((u - 0xD800u) << 10) | (nx - 0xDC00u));
-          d[q] = (uint8_t)(0xF0u | (cp >> 18));
-          d[q + 1] = (uint8_t)(0x80u | ((cp >> 12) & 0x3Fu));
-          d[q + 2] = (uint8_t)(0x80u | ((cp >> 6) & 0x3Fu));
-          d[q + 3] = (uint8_t)(0x80u | (cp & 0x3Fu));
-          q += 4;
-        } else if (!is_lo(u)) {
-          d[q] = (uint8_t)(0xE0u | (u >> 12));
-          d[q + 1] = (uint8_t)(0x80u | ((u >> 6) & 0x3Fu));
-          d[q + 2] = (uint8_t)(0x80u | (u & 0x3Fu));
-          q += 3;
-        }
-      }
-    }
-    __syncthreads();
-    const unsigned long long excl = sm.excl;
-    if (excl != ~0ull) copy_out(a.out + excl, sm.out, agg, U16_THREADS);
-    __syncthreads();
+    if (dst)
+      for (unsigned b = 0; b < len; b++) dst[q + b] = (uint8_t)(p >> (8 * b));
+    q += len;
   }
-  // last CTA writes the result and re-arms the control block
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&a.ctl->done, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence();
-      const unsigned long long e = load_relaxed(&a.ctl->err);
-      vt_result r;
-      if (kTranscode) {
-        const unsigned t = e == kNoError ? a.ntiles - 1 : (unsigned)((e + a.head) / U16_TILE);
-        r.written = load_status(&a.status[t]) & kValMask;
-      } else {
-        r.written = load_relaxed(&a.ctl->count);
-      }
-      r.consumed = e == kNoError ? a.n : e;
-      r.error_at = e == kNoError ? -1 : (long long)e;
-      *a.res = r;
-      a.ctl->tile_counter = 0;
-      a.ctl->count = 0;
-      a.ctl->err = kNoError;
-      __threadfence();
-      a.ctl->done = 0;
+  return q;
+}
+
+struct TileCount16 {
+  Words16 W;
+  long long v0;
+  unsigned lo, lim;
+  bool simple;
+  unsigned cnt;
+};
+
+struct Class16 {
+  unsigned bytes, chars;
+  bool err;
+};
+
+// Phase A over the 16 own words: pairing check and counts (SWAR, 16-bit lanes).
+__device__ __forceinline__ Class16 classify16(const Words16& W) {
+  uint32_t hp, lp;  // surrogate planes of the previous word
+  {
+    const uint32_t x = W.w[0];
+    hp = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;
+    lp = ~nz_hi6((x & 0xFC00FC00u) ^ 0xDC00DC00u) & H16;
+  }
+  uint32_t hcur = 0, lcur = 0;
+  uint32_t err = 0, acc = 0, nlo = 0;
+#pragma unroll
+  for (int k = 1; k <= K16_WPT + 1; k++) {
+    const uint32_t x = W.w[k];
+    const uint32_t hm = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;
+    const uint32_t lm = ~nz_hi6((x & 0xFC00FC00u) ^ 0xDC00DC00u) & H16;
+    if (k >= 2) {
+      // word k-1: its units' predecessors and successors
+      const uint32_t prev_hi = __funnelshift_l(hp, hcur, 16);
+      const uint32_t next_lo = __funnelshift_r(lcur, lm, 16);
+      err |= (lcur & ~prev_hi) | (hcur & ~next_lo);
+      hp = hcur;
+    }
+    if (k <= K16_WPT) {
+      const uint32_t g80 = ((((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16) >> 15;
+      const uint32_t g800 = ((((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16) >> 15;
+      acc += g80 + g800 + (hm >> 15);
+      nlo += lm >> 15;
+      hcur = hm;
+      lcur = lm;
     }
   }
+  (void)lp;
+  Class16 c;
+  const unsigned a = (acc & 0xFFFFu) + (acc >> 16), l = (nlo & 0xFFFFu) + (nlo >> 16);
+  c.bytes = K16_UPT + a - 3 * l;
+  c.chars = K16_UPT - l;
+  c.err = err != 0;
+  return c;
+}
+
+template <bool kTranscode, int NT, class Sync>
+__device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, unsigned* red,
+                                             unsigned* scan, TileCount16& tc, unsigned& off,
+                                             unsigned& agg) {
+  const unsigned lane = threadIdx.x & 31;
+  const long long vt0 = (long long)tile * K16_TILE;
+  tc.v0 = vt0 + (long long)K16_UPT * threadIdx.x;
+  const Src16 src{a.base, a.head, a.n};
+  const bool interior =
+      vt0 - 2 >= (long long)a.head && vt0 + K16_TILE + 2 <= (long long)(a.head + a.n);
+  if (interior) {
+    const uint4* p = reinterpret_cast<const uint4*>(a.base + tc.v0);
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const uint4 v = __ldg(p + r);
+      tc.W.w[1 + 4 * r] = v.x; tc.W.w[2 + 4 * r] = v.y;
+      tc.W.w[3 + 4 * r] = v.z; tc.W.w[4 + 4 * r] = v.w;
+    }
+    uint32_t pw = __shfl_up_sync(0xffffffffu, tc.W.w[K16_WPT], 1);
+    uint32_t nw = __shfl_down_sync(0xffffffffu, tc.W.w[1], 1);
+    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 - 2));
+    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 + K16_UPT));
+    tc.W.w[0] = pw;
+    tc.W.w[K16_WPT + 1] = nw;
+  } else {
+    Words16 L;
+    load_masked16(src, tc.v0, L);
+#pragma unroll
+    for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = L.w[k];
+  }
+  const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
+  tc.lo = (unsigned)max(0LL, min((long long)K16_UPT, s));
+  const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K16_UPT, e));
+  tc.lim = hi;
+  const Class16 c = classify16(tc.W);
+  unsigned my_err = kNone16;
+  if (c.err || !interior) {
+    const unsigned er = first_error16(src, tc.v0, tc.lo, hi);
+    if (er != kNone16) my_err = K16_UPT * threadIdx.x + er;
+  }
+  if (interior) {
+    static_assert(NT <= 256 && 4 * K16_TILE < (1 << 23), "packed scan fields");
+    tc.cnt = kTranscode ? c.bytes : c.chars;
+    unsigned total;
+    off = block_excl_scan<NT, Sync, false>(my_err == kNone16 ? tc.cnt : (1u << 23), scan, total);
+    if ((total >> 23) == 0) {
+      tc.simple = true;
+      agg = total;
+      return;
+    }
+  }
+  const unsigned tile_err = block_min<NT, Sync>(my_err, red);
+  tc.simple = false;
+  if (tile_err != kNone16) {
+    const unsigned start = K16_UPT * threadIdx.x;
+    tc.lim = max(tc.lo, min(hi, tile_err <= start ? 0u : tile_err - start));
+    if (threadIdx.x == 0) {
+      const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
+      atomicMin(&a.ctl->err, pos);
+    }
+  }
+  tc.cnt = generic_units(src, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
+  off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
+}
+
+// Encode one word (two units) at the running shared address q.
+__device__ __forceinline__ void emit_word16(uint32_t x, uint32_t nxw, uint32_t& q) {
+  if ((x & 0xFF80FF80u) == 0) {  // two ASCII units
+    sts8(q, x);
+    sts8(q + 1, x >> 16);
+    q += 2;
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const unsigned u = h ? (x >> 16) : (x & 0xFFFFu);
+    const unsigned nx = h ? (nxw & 0xFFFFu) : (x >> 16);
+    unsigned len;
+    const uint32_t p = encode_unit(u, nx, len);
+    if (len >= 1) sts8(q, p);
+    if (len >= 2) sts8(q + 1, p >> 8);
+    if (len >= 3) sts8(q + 2, p >> 16);
+    if (len >= 4) sts8(q + 3, p >> 24);
+    q += len;
+  }
+}
+
+struct Utf16Codec {
+  using Args = U16Args;
+  using TileCount = TileCount16;
+  static constexpr int kTileElems = K16_TILE;
+  static constexpr int kStageBytes = 3 * K16_TILE;
+  static constexpr int kOutBytes = 1;
+  template <bool kTranscode, int NT, class Sync>
+  __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
+                                               unsigned* scan, TileCount& tc, unsigned& off,
+                                               unsigned& agg) {
+    count_tile16<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg);
+  }
+  __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
+                                              unsigned off) {
+    if (tc.simple) {
+      uint32_t q = smem_addr(stage) + off;
+#pragma unroll
+      for (int k = 1; k <= K16_WPT; k++) emit_word16(tc.W.w[k], tc.W.w[k + 1], q);
+    } else {
+      generic_units(Src16{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kComputeThreads, 4) utf16_validate_kernel(U16Args a) {
+  validate_body<Utf16Codec>(a);
+}
+
+__global__ void __launch_bounds__(kPipeBlock, 3) utf16_transcode_kernel(U16Args a) {
+  extern __shared__ __align__(16) uint8_t k16_dyn_smem[];
+  transcode_body<Utf16Codec>(a, *reinterpret_cast<PipeSmem<Utf16Codec>*>(k16_dyn_smem));
+}
+
+static int set_smem_attr16() {
+  return (int)cudaFuncSetAttribute(utf16_transcode_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sizeof(PipeSmem<Utf16Codec>));
 }
 
 int launch_utf16(const U16Args& a, bool transcode, int grid, cudaStream_t s) {
+  static const int attr_rc = set_smem_attr16();
+  if (attr_rc) return attr_rc;
   if (transcode)
-    utf16_kernel<true><<<grid, U16_THREADS, 0, s>>>(a);
+    utf16_transcode_kernel<<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec>), s>>>(a);
   else
-    utf16_kernel<false><<<grid, U16_THREADS, 0, s>>>(a);
+    utf16_validate_kernel<<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
 int occupancy_utf16(bool transcode) {
   int n = 0;
-  if (transcode)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_kernel<true>, U16_THREADS, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_kernel<false>, U16_THREADS, 0);
+  if (transcode) {
+    if (set_smem_attr16()) return 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_transcode_kernel, kPipeBlock,
+                                                  sizeof(PipeSmem<Utf16Codec>));
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_validate_kernel, kComputeThreads, 0);
+  }
   return n;
 }
 
 unsigned tiles_utf16(unsigned long long head, unsigned long long n) {
-  const unsigned long long t = (head + n + U16_TILE - 1) / U16_TILE;
+  const unsigned long long t = (head + n + K16_TILE - 1) / K16_TILE;
   return (unsigned)(t ? t : 1);
 }
 

@@ -25,12 +25,12 @@
 // and tiles containing an error take a simple masked per-character path.
 #include <cstdio>
 
-#include "vt_device.cuh"
 #include "vt_kernels.h"
+#include "vt_pipeline.cuh"
 
 namespace vt {
 
-constexpr int K8_THREADS = 256;
+constexpr int K8_THREADS = kComputeThreads;
 constexpr int K8_WPT = 16;                      // words per thread
 constexpr int K8_BPT = 4 * K8_WPT;              // bytes per thread
 constexpr int K8_TILE = K8_THREADS * K8_BPT;    // bytes per tile
@@ -153,24 +153,22 @@ __device__ __forceinline__ void load_interior(const uint8_t* p, Words& W) {
   W.w[K8_WPT + 1] = __ldg(reinterpret_cast<const uint32_t*>(p + K8_BPT));
 }
 
-// Exact range check of every suspicious lead (interior tiles; reloads the
-// window, which is still in L1/L2); true if one is malformed.
-__device__ __noinline__ bool susp_fail(const uint8_t* p) {
-  Words W;
-  load_interior(p, W);
-  for (int k = 0; k < K8_WPT; k++) {
-    uint32_t m = susp_lanes(W.w[k + 1]);
-    while (m) {
-      const unsigned lanebit = __ffs(m) - 1;  // 7, 15, 23 or 31
-      m &= m - 1;
-      const uint32_t v = __funnelshift_r(W.w[k + 1], W.w[k + 2], lanebit - 7);
-      if (!decode_ok(v)) return true;
-    }
+// Exact range check of the leads flagged in m (bit 7 of each lane) of word x,
+// followed by word nx; true if one of them does not decode.
+__device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) {
+  bool bad = false;
+  while (m) {
+    const unsigned lanebit = __ffs(m) - 1;  // 7, 15, 23 or 31
+    m &= m - 1;
+    if (!decode_ok(__funnelshift_r(x, nx, lanebit - 7))) bad = true;
   }
-  return false;
+  return bad;
 }
 
-// Phase A over the 16 own words (SWAR, no branches).
+// Phase A over the 16 own words (SWAR).  Leads whose value range depends on
+// the next byte (C0 C1 / E0 ED, with EE EF as harmless extras / F0 F4..FF) are
+// flagged with a few bit operations and checked exactly right away; they are
+// rare in most text, so the check is a short, register-only branch.
 __device__ __forceinline__ ClassOut classify(const Words& W) {
   uint32_t p2, p3, p4;
   {
@@ -179,7 +177,8 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
     p3 = p2 & (x << 2);
     p4 = p3 & (x << 3);
   }
-  uint32_t viol = 0, susp = 0, ccont = 0, cfour = 0;
+  uint32_t viol = 0, ccont = 0, cfour = 0;
+  bool range_bad = false, susp_any = false;
 #pragma unroll
   for (int k = 1; k <= K8_WPT + 1; k++) {
     const uint32_t x = W.w[k], x2 = x << 1;
@@ -196,7 +195,17 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
       const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
       const uint32_t y = x & 0x1E1E1E1Eu;
       const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
-      susp |= z3 | z2;
+      uint32_t susp = z3 | z2;
+      if (l4) {
+        // 4-byte leads other than F1..F3
+        const uint32_t ln = x & 0x0F0F0F0Fu;
+        const uint32_t ok = (ln + 0x7F7F7F7Fu) & ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);
+        susp |= l4 & ~ok;
+      }
+      if (susp) {
+        susp_any = true;
+        if (lanes_fail(susp, x, W.w[k + 1])) range_bad = true;
+      }
       ccont += c >> 7;
       cfour += l4 >> 7;
     } else {
@@ -208,8 +217,8 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
   const unsigned nc = (ccont * 0x01010101u) >> 24, n4 = (cfour * 0x01010101u) >> 24;
   o.chars = K8_BPT - nc;
   o.units = o.chars + n4;
-  o.viol = viol != 0;
-  o.susp = susp != 0;
+  o.viol = viol != 0 || range_bad;
+  o.susp = susp_any;
   o.four = n4 != 0;
   return o;
 }
@@ -247,27 +256,6 @@ __device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
     }
   }
   return q;
-}
-
-// 4-byte leads whose value range needs the second byte: F0, F4..FF (only
-// F1..F3 are always in range).  Interior tiles; reloads the window.
-__device__ __noinline__ bool four_fail(const uint8_t* p) {
-  Words W;
-  load_interior(p, W);
-  for (int k = 1; k <= K8_WPT; k++) {
-    const uint32_t x = W.w[k];
-    const uint32_t l4 = x & (x << 1) & (x << 2) & (x << 3) & H;
-    const uint32_t ln = x & 0x0F0F0F0Fu;
-    const uint32_t nz = ln + 0x7F7F7F7Fu;                       // bit 7: ln != 0
-    const uint32_t lt4 = ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);   // bit 7: ln < 4
-    uint32_t m = l4 & ~(nz & lt4);
-    while (m) {
-      const unsigned lanebit = __ffs(m) - 1;
-      m &= m - 1;
-      if (!decode_ok(__funnelshift_r(x, W.w[k + 1], lanebit - 7))) return true;
-    }
-  }
-  return false;
 }
 
 // Branch-free decode of one word: lead-attributed byte planes of each
@@ -369,8 +357,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   tc.four = co.four;
   tc.lim = hi;
   unsigned my_err = kNone;
-  if (co.viol || !interior || (co.susp && susp_fail(a.base + tc.v0)) ||
-      (co.four && four_fail(a.base + tc.v0))) {
+  if (co.viol || !interior) {
     const unsigned er = first_error_rule_a(src, tc.v0, tc.lo, hi);
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
@@ -419,167 +406,46 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
   }
 }
 
-__device__ __forceinline__ void finalize_if_last(const U8Args& a, bool transcode) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(&a.ctl->done, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence();
-      const unsigned long long e = load_relaxed(&a.ctl->err);
-      vt_result r;
-      if (transcode) {
-        const unsigned t = e == kNoError ? a.ntiles - 1 : (unsigned)((e + a.head) / K8_TILE);
-        r.written = load_status(&a.status[t]) & kValMask;
-      } else {
-        r.written = load_relaxed(&a.ctl->count);
-      }
-      r.consumed = e == kNoError ? a.n : e;
-      r.error_at = e == kNoError ? -1 : (long long)e;
-      *a.res = r;
-      a.ctl->tile_counter = 0;
-      a.ctl->count = 0;
-      a.ctl->err = kNoError;
-      __threadfence();
-      a.ctl->done = 0;
-    }
+struct Utf8Codec {
+  using Args = U8Args;
+  using TileCount = vt::TileCount;
+  static constexpr int kTileElems = K8_TILE;
+  static constexpr int kStageBytes = 2 * K8_TILE;
+  static constexpr int kOutBytes = 2;
+  template <bool kTranscode, int NT, class Sync>
+  __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
+                                               unsigned* scan, TileCount& tc, unsigned& off,
+                                               unsigned& agg) {
+    count_tile<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg);
   }
-}
-
-// Next tile for this CTA (thread 0).  Tiles are taken in order, one at a time
-// per CTA, so look-back never waits for a tile nobody has started; tiles
-// behind a known error are skipped (the reference stops there too).
-__device__ __forceinline__ unsigned grab_tile(const U8Args& a) {
-  unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
-  const unsigned long long e = load_relaxed(&a.ctl->err);
-  if (t < a.ntiles && e != kNoError && (e + a.head) / K8_TILE < t) t = a.ntiles;
-  return t;
-}
-
-// ---- validation / counting: no output, no look-back -----------------------------
-__global__ void __launch_bounds__(K8_THREADS, 4) utf8_validate_kernel(U8Args a) {
-  __shared__ unsigned red[K8_THREADS / 32], scan[K8_THREADS / 32];
-  __shared__ unsigned tile_s;
-  while (true) {
-    if (threadIdx.x == 0) tile_s = grab_tile(a);
-    __syncthreads();
-    const unsigned tile = tile_s;
-    if (tile >= a.ntiles) break;
-    TileCount tc;
-    unsigned off, total;
-    count_tile<false, K8_THREADS, SyncAll>(a, tile, red, scan, tc, off, total);
-    if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
+  __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
+                                              unsigned off) {
+    emit_tile(a, tc, reinterpret_cast<uint16_t*>(stage), off);
   }
-  finalize_if_last(a, false);
-}
-
-// ---- transcoding: warp-specialised pipeline ----------------------------------------
-// Warps 0..7 (compute) count tile j, hand its aggregate to warp 8 (look-back),
-// decode it into staging buffer j%2, and copy tile j-1 out once warp 8 has
-// resolved its offset.  The look-back latency is hidden behind a whole tile.
-constexpr int K8_BLOCK = K8_THREADS + 32;
-constexpr int BAR_COMPUTE = 1, BAR_AGG = 2, BAR_EXCL = 3;
-constexpr unsigned kSentinel = 0xFFFFFFFFu;
-using ComputeSync = SyncNamed<BAR_COMPUTE, K8_THREADS>;
-
-struct K8TSmem {
-  alignas(16) uint8_t pad0[32];
-  alignas(16) uint16_t out[2][K8_TILE + 16];
-  alignas(16) uint8_t pad1[32];
-  unsigned scan[K8_THREADS / 32];
-  unsigned red[K8_THREADS / 32];
-  unsigned tile;
-  unsigned agg_tile[2], agg[2];
-  unsigned long long excl[2];
 };
 
-__global__ void __launch_bounds__(K8_BLOCK, 3) utf8_transcode_kernel(U8Args a) {
+__global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Args a) {
+  validate_body<Utf8Codec>(a);
+}
+
+__global__ void __launch_bounds__(kPipeBlock, 3) utf8_transcode_kernel(U8Args a) {
   extern __shared__ __align__(16) uint8_t k8_dyn_smem[];
-  K8TSmem& sm = *reinterpret_cast<K8TSmem*>(k8_dyn_smem);
-  if (threadIdx.x >= K8_THREADS) {
-    // look-back warp
-    for (unsigned j = 0;; j++) {
-      bar_sync(BAR_AGG, K8_BLOCK);
-      const unsigned tile = sm.agg_tile[j & 1];
-      if (tile == kSentinel) break;
-      const unsigned agg = sm.agg[j & 1];
-      unsigned long long excl = 0;
-      if (tile == 0) {
-        if (threadIdx.x == K8_THREADS) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
-      } else {
-        if (threadIdx.x == K8_THREADS)
-          store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
-        excl = lookback(a.status, a.epoch, tile, a.ctl, K8_TILE, a.head);
-        if (threadIdx.x == K8_THREADS && excl != ~0ull)
-          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
-      }
-      if (threadIdx.x == K8_THREADS) sm.excl[j & 1] = excl;
-      __syncwarp();
-      bar_arrive(BAR_EXCL, K8_BLOCK);
-    }
-  } else {
-    // compute warps
-    if (threadIdx.x == 0) sm.tile = grab_tile(a);
-    unsigned j = 0, prev_agg = 0;
-    while (true) {
-      ComputeSync::sync();
-      const unsigned tile = sm.tile;
-      if (tile >= a.ntiles) break;
-      TileCount tc;
-      unsigned off, agg;
-      count_tile<true, K8_THREADS, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
-      if (j > 0) {
-        // tile j-1: wait for its offset, then copy it out
-        bar_sync(BAR_EXCL, K8_BLOCK);
-        const unsigned long long excl = sm.excl[(j - 1) & 1];
-        if (a.dbg & 4) {
-          if (threadIdx.x == 0) printf("tile %u j %u excl %llu prev_agg %u\n", tile, j, excl, prev_agg);
-        }
-        if (excl != ~0ull && !(a.dbg & 2))
-          copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
-                   reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
-      }
-      if (threadIdx.x == 0) {
-        sm.agg_tile[j & 1] = tile;
-        sm.agg[j & 1] = agg;
-      }
-      bar_arrive(BAR_AGG, K8_BLOCK);
-      if (a.dbg & 4) {
-        if (threadIdx.x == 0) printf("tile %u agg %u simple0 %d\n", tile, agg, (int)tc.simple);
-      }
-      if (!(a.dbg & 1)) emit_tile(a, tc, sm.out[j & 1], off);
-      if (threadIdx.x == 0) sm.tile = grab_tile(a);
-      prev_agg = agg;
-      j++;
-    }
-    if (j > 0) {
-      bar_sync(BAR_EXCL, K8_BLOCK);
-      const unsigned long long excl = sm.excl[(j - 1) & 1];
-      if (a.dbg & 4) {
-        if (threadIdx.x == 0) printf("final j %u excl %llu prev_agg %u\n", j, excl, prev_agg);
-      }
-      if (excl != ~0ull && !(a.dbg & 2))
-        copy_out(reinterpret_cast<uint8_t*>(a.out + excl),
-                 reinterpret_cast<const uint8_t*>(sm.out[(j - 1) & 1]), 2u * prev_agg, K8_THREADS);
-    }
-    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
-    bar_arrive(BAR_AGG, K8_BLOCK);
-  }
-  finalize_if_last(a, true);
+  transcode_body<Utf8Codec>(a, *reinterpret_cast<PipeSmem<Utf8Codec>*>(k8_dyn_smem));
 }
 
 static int set_smem_attr() {
   return (int)cudaFuncSetAttribute(utf8_transcode_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(K8TSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sizeof(PipeSmem<Utf8Codec>));
 }
 
 int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s) {
   static const int attr_rc = set_smem_attr();
   if (attr_rc) return attr_rc;
   if (transcode)
-    utf8_transcode_kernel<<<grid, K8_BLOCK, sizeof(K8TSmem), s>>>(a);
+    utf8_transcode_kernel<<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec>), s>>>(a);
   else
-    utf8_validate_kernel<<<grid, K8_THREADS, 0, s>>>(a);
+    utf8_validate_kernel<<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -587,11 +453,11 @@ int occupancy_utf8(bool transcode) {
   int n = 0;
   if (transcode) {
     if (set_smem_attr()) return 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel, K8_BLOCK,
-                                                  sizeof(K8TSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel, kPipeBlock,
+                                                  sizeof(PipeSmem<Utf8Codec>));
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel, kComputeThreads, 0);
   }
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel, K8_THREADS, 0);
   return n;
 }
 

@@ -1,0 +1,171 @@
+// vt_pipeline.cuh -- the tile pipeline shared by both transcoding directions.
+//
+// A Codec supplies the per-tile work:
+//   using Args;  (fields: base, head, n, ntiles, epoch, out, status, ctl, res)
+//   using TileCount;
+//   kTileElems  input elements (bytes / units) per tile
+//   kStageBytes largest output of one tile, in bytes
+//   kOutBytes   bytes per output element (2 for UTF-16, 1 for UTF-8)
+//   count<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg)
+//       load + validate + count the tile; off = this thread's exclusive
+//       output offset, agg = the tile's output (elements); errors reported
+//       through atomicMin(&ctl->err) and clipped out of the counts
+//   emit(a, tc, stage, off)  write this thread's output at stage + off
+//
+// Two kernels are built from it:
+//   validate_body: count only; the code-point total goes to ctl->count;
+//   transcode_body: warp-specialised.  Warps 0..7 count tile j, hand its
+//       aggregate to warp 8, decode tile j into staging buffer j%2 and copy
+//       tile j-1 to global memory once warp 8 has resolved its offset with
+//       the decoupled look-back.  The look-back latency hides behind a whole
+//       tile of work.  Tiles are taken in order, one at a time per CTA.
+#pragma once
+
+#include "vt_device.cuh"
+
+namespace vt {
+
+constexpr int kComputeThreads = 256;
+constexpr int kPipeBlock = kComputeThreads + 32;
+constexpr int BAR_COMPUTE = 1, BAR_AGG = 2, BAR_EXCL = 3;
+constexpr unsigned kSentinel = 0xFFFFFFFFu;
+using ComputeSync = SyncNamed<BAR_COMPUTE, kComputeThreads>;
+
+template <class Args>
+__device__ __forceinline__ void finalize_if_last(const Args& a, bool transcode,
+                                                 unsigned tile_elems) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&a.ctl->done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long e = load_relaxed(&a.ctl->err);
+      vt_result r;
+      if (transcode) {
+        // written = inclusive prefix of the last tile, or of the tile holding
+        // the first error (its aggregate stops at that error)
+        const unsigned t = e == kNoError ? a.ntiles - 1 : (unsigned)((e + a.head) / tile_elems);
+        r.written = load_status(&a.status[t]) & kValMask;
+      } else {
+        r.written = load_relaxed(&a.ctl->count);
+      }
+      r.consumed = e == kNoError ? a.n : e;
+      r.error_at = e == kNoError ? -1 : (long long)e;
+      *a.res = r;
+      a.ctl->tile_counter = 0;
+      a.ctl->count = 0;
+      a.ctl->err = kNoError;
+      __threadfence();
+      a.ctl->done = 0;
+    }
+  }
+}
+
+// Next tile for this CTA (called by one thread).  Tiles behind a known error
+// are skipped: their output can never be read (the reference stops there too).
+template <class Args>
+__device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems) {
+  unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
+  const unsigned long long e = load_relaxed(&a.ctl->err);
+  if (t < a.ntiles && e != kNoError && (e + a.head) / tile_elems < t) t = a.ntiles;
+  return t;
+}
+
+template <class C>
+__device__ __forceinline__ void validate_body(const typename C::Args& a) {
+  __shared__ unsigned red[kComputeThreads / 32], scan[kComputeThreads / 32];
+  __shared__ unsigned tile_s;
+  while (true) {
+    if (threadIdx.x == 0) tile_s = grab_tile(a, C::kTileElems);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    if (tile >= a.ntiles) break;
+    typename C::TileCount tc;
+    unsigned off, total;
+    C::template count<false, kComputeThreads, SyncAll>(a, tile, red, scan, tc, off, total);
+    if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
+  }
+  finalize_if_last(a, false, C::kTileElems);
+}
+
+template <class C>
+struct PipeSmem {
+  alignas(16) uint8_t pad0[32];
+  alignas(16) uint8_t out[2][C::kStageBytes + 32];
+  alignas(16) uint8_t pad1[32];
+  unsigned scan[kComputeThreads / 32];
+  unsigned red[kComputeThreads / 32];
+  unsigned tile;
+  unsigned agg_tile[2], agg[2];
+  unsigned long long excl[2];
+};
+
+template <class C>
+__device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const uint8_t* stage,
+                                              unsigned long long excl, unsigned agg) {
+  if (excl == ~0ull) return;  // a tile before this one failed: output is dead
+  copy_out(reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes, stage, agg * C::kOutBytes,
+           kComputeThreads);
+}
+
+template <class C>
+__device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
+  if (threadIdx.x >= kComputeThreads) {
+    // look-back warp
+    const bool leader = threadIdx.x == kComputeThreads;
+    for (unsigned j = 0;; j++) {
+      bar_sync(BAR_AGG, kPipeBlock);
+      const unsigned tile = sm.agg_tile[j & 1];
+      if (tile == kSentinel) break;
+      const unsigned agg = sm.agg[j & 1];
+      unsigned long long excl = 0;
+      if (tile == 0) {
+        if (leader) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
+      } else {
+        if (leader) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
+        excl = lookback(a.status, a.epoch, tile, a.ctl, C::kTileElems, a.head);
+        if (leader && excl != ~0ull)
+          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
+      }
+      if (leader) sm.excl[j & 1] = excl;
+      __syncwarp();
+      bar_arrive(BAR_EXCL, kPipeBlock);
+    }
+  } else {
+    // compute warps
+    if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
+    unsigned j = 0, prev_agg = 0;
+    while (true) {
+      ComputeSync::sync();
+      const unsigned tile = sm.tile;
+      if (tile >= a.ntiles) break;
+      typename C::TileCount tc;
+      unsigned off, agg;
+      C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
+      if (j > 0) {
+        // tile j-1: wait for its offset (resolved meanwhile), copy it out
+        bar_sync(BAR_EXCL, kPipeBlock);
+        copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
+      }
+      if (threadIdx.x == 0) {
+        sm.agg_tile[j & 1] = tile;
+        sm.agg[j & 1] = agg;
+      }
+      bar_arrive(BAR_AGG, kPipeBlock);
+      C::emit(a, tc, sm.out[j & 1], off);
+      if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
+      prev_agg = agg;
+      j++;
+    }
+    if (j > 0) {
+      bar_sync(BAR_EXCL, kPipeBlock);
+      copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
+    }
+    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
+    bar_arrive(BAR_AGG, kPipeBlock);
+  }
+  finalize_if_last(a, true, C::kTileElems);
+}
+
+}  // namespace vt
