@@ -243,6 +243,25 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
+// Branch-free UTF-8 encoding of one unit u (followed by nx): the bytes,
+// little-endian, and their number (0 for the low half of a pair).
+__device__ __forceinline__ uint32_t encode_unit_bf(uint32_t u, uint32_t nx, uint32_t& len) {
+  const uint32_t g80 = u >= 0x80u, g800 = u >= 0x800u;
+  const uint32_t top6 = u >> 10;  // 0x36: high surrogate, 0x37: low surrogate
+  const uint32_t hs = top6 == 0x36u, ls = top6 == 0x37u;
+  // 2- and 3-byte forms (used for every BMP unit, selected by g800)
+  const uint32_t p2 = 0x80C0u | (u >> 6) | ((u << 8) & 0x3F00u);
+  const uint32_t p3 = 0x8080E0u | (u >> 12) | ((u << 2) & 0x3F00u) | ((u << 16) & 0x3F0000u);
+  // 4-byte form of the pair (u, nx)
+  const uint32_t cp = 0x10000u + (((u & 0x3FFu) << 10) | (nx & 0x3FFu));
+  const uint32_t p4 = 0x808080F0u | (cp >> 18) | ((cp >> 4) & 0x3F00u) | ((cp << 10) & 0x3F0000u) |
+                      ((cp << 24) & 0x3F000000u);
+  uint32_t p = g800 ? p3 : (g80 ? p2 : u);
+  p = hs ? p4 : p;
+  len = ls ? 0u : 1u + g80 + g800 + hs;
+  return p;
+}
+
 // Encode one word (two units) at the running shared address q.
 __device__ __forceinline__ void emit_word16(uint32_t x, uint32_t nxw, uint32_t& q) {
   if ((x & 0xFF80FF80u) == 0) {  // two ASCII units
@@ -253,10 +272,10 @@ __device__ __forceinline__ void emit_word16(uint32_t x, uint32_t nxw, uint32_t& 
   }
 #pragma unroll
   for (int h = 0; h < 2; h++) {
-    const unsigned u = h ? (x >> 16) : (x & 0xFFFFu);
-    const unsigned nx = h ? (nxw & 0xFFFFu) : (x >> 16);
-    unsigned len;
-    const uint32_t p = encode_unit(u, nx, len);
+    const uint32_t u = h ? (x >> 16) : (x & 0xFFFFu);
+    const uint32_t nx = h ? (nxw & 0xFFFFu) : (x >> 16);
+    uint32_t len;
+    const uint32_t p = encode_unit_bf(u, nx, len);
     if (len >= 1) sts8(q, p);
     if (len >= 2) sts8(q + 1, p >> 8);
     if (len >= 3) sts8(q + 2, p >> 16);
