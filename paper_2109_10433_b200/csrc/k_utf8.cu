@@ -165,10 +165,39 @@ __device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) 
   return bad;
 }
 
-// Phase A over the 16 own words (SWAR).  Leads whose value range depends on
-// the next byte (C0 C1 / E0 ED, with EE EF as harmless extras / F0 F4..FF) are
-// flagged with a few bit operations and checked exactly right away; they are
-// rare in most text, so the check is a short, register-only branch.
+// Leads whose value range depends on the next byte, as bit 7 of each lane:
+// C0 C1 (x & 0x1E == 0 among 2-byte leads), E0 ED (+ EE EF, harmless extras:
+// ((nibble + 3) & 0xC) == 0 among 3-byte leads), and 4-byte leads other than
+// F1..F3 (only F0 and F4 depend on the next byte; F5..FF are always invalid).
+__device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint32_t l3,
+                                                  uint32_t l4) {
+  const uint32_t ln = x & 0x0F0F0F0Fu;
+  const uint32_t t = ln + 0x03030303u;
+  const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
+  const uint32_t y = x & 0x1E1E1E1Eu;
+  const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
+  const uint32_t f_ok = (ln + 0x7F7F7F7Fu) & ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);  // ln in 1..3
+  return (z3 | z2 | (l4 & ~f_ok)) & H;
+}
+
+// Exact range check of the special leads of every word (only threads whose
+// bytes contain such a lead get here; registers only).
+__device__ __forceinline__ bool specials_fail(const Words& W) {
+  bool bad = false;
+#pragma unroll
+  for (int k = 1; k <= K8_WPT; k++) {
+    const uint32_t x = W.w[k], x2 = x << 1;
+    const uint32_t l2 = x & x2 & H;
+    const uint32_t l3 = l2 & (x << 2);
+    const uint32_t l4 = l3 & (x << 3);
+    const uint32_t m = special_lanes(x, l2, l3, l4);
+    if (m && lanes_fail(m, x, W.w[k + 1])) bad = true;
+  }
+  return bad;
+}
+
+// Phase A over the 16 own words (SWAR, branch-free): structure check,
+// special-lead flag, counts.
 __device__ __forceinline__ ClassOut classify(const Words& W) {
   uint32_t p2, p3, p4;
   {
@@ -177,35 +206,19 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
     p3 = p2 & (x << 2);
     p4 = p3 & (x << 3);
   }
-  uint32_t viol = 0, ccont = 0, cfour = 0;
-  bool range_bad = false, susp_any = false;
+  uint32_t viol = 0, spec = 0, ccont = 0, cfour = 0;
 #pragma unroll
   for (int k = 1; k <= K8_WPT + 1; k++) {
-    const uint32_t x = W.w[k], x2 = x << 1;
+    const uint32_t x = W.w[k], x2 = x << 1, x8 = x << 3;
     const uint32_t c = x & ~x2 & H;
     const uint32_t l2 = x & x2 & H;
     const uint32_t l3 = l2 & (x << 2);
-    const uint32_t l4 = l3 & (x << 3);
+    const uint32_t l4 = l3 & x8;
     const uint32_t need = __funnelshift_l(p2, l2, 8) | __funnelshift_l(p3, l3, 16) |
                           __funnelshift_l(p4, l4, 24);
     if (k <= K8_WPT) {
       viol |= need ^ c;
-      // E0 ED EE EF: ((low nibble + 3) & 0xC) == 0 ; C0 C1: (x & 0x1E) == 0
-      const uint32_t t = (x & 0x0F0F0F0Fu) + 0x03030303u;
-      const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
-      const uint32_t y = x & 0x1E1E1E1Eu;
-      const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
-      uint32_t susp = z3 | z2;
-      if (l4) {
-        // 4-byte leads other than F1..F3
-        const uint32_t ln = x & 0x0F0F0F0Fu;
-        const uint32_t ok = (ln + 0x7F7F7F7Fu) & ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);
-        susp |= l4 & ~ok;
-      }
-      if (susp) {
-        susp_any = true;
-        if (lanes_fail(susp, x, W.w[k + 1])) range_bad = true;
-      }
+      spec |= special_lanes(x, l2, l3, l4);
       ccont += c >> 7;
       cfour += l4 >> 7;
     } else {
@@ -217,8 +230,8 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
   const unsigned nc = (ccont * 0x01010101u) >> 24, n4 = (cfour * 0x01010101u) >> 24;
   o.chars = K8_BPT - nc;
   o.units = o.chars + n4;
-  o.viol = viol != 0 || range_bad;
-  o.susp = susp_any;
+  o.viol = (viol & H) != 0 || ((spec & H) != 0 && specials_fail(W));
+  o.susp = (spec & H) != 0;
   o.four = n4 != 0;
   return o;
 }
