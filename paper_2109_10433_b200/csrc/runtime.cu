@@ -22,6 +22,9 @@
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
+extern "C" uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut);
+extern "C" uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut);
+
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
@@ -244,6 +247,18 @@ struct HostCtx {
   uint8_t* d_in = nullptr;
   uint8_t* d_out = nullptr;
   size_t d_in_cap = 0, d_out_cap = 0;
+  // chunked pipeline (large host-pointer calls): kPipeBufs streams and buffers
+  static constexpr int kPipeBufs = 3;
+  cudaStream_t ps[kPipeBufs] = {};
+  cudaEvent_t pev[kPipeBufs] = {};
+  uint8_t* pd_in[kPipeBufs] = {};
+  uint8_t* pd_out[kPipeBufs] = {};
+  size_t pd_in_cap = 0, pd_out_cap = 0;
+  vt_result* pd_res = nullptr;   // kPipeBufs slots, device
+  vt_result* ph_res = nullptr;   // kPipeBufs slots, pinned host
+  uint8_t* ph_in[kPipeBufs] = {};   // pinned staging for pageable callers
+  uint8_t* ph_out[kPipeBufs] = {};
+  size_t ph_in_cap = 0, ph_out_cap = 0;
   ~HostCtx() {
     // process teardown: the driver reclaims everything; avoid CUDA calls here
   }
@@ -279,6 +294,137 @@ int ensure_dev(uint8_t*& p, size_t& cap, size_t need, cudaStream_t s) {
   return 0;
 }
 
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+int ensure_pinned(uint8_t*& p, size_t& cap, size_t need) {
+  if (need <= cap && p) return 0;
+  if (p) VT_TRY(cudaFreeHost(p));
+  VT_TRY(cudaMallocHost(&p, need));
+  cap = need;
+  return 0;
+}
+
+// Input elements per pipeline chunk (64 MiB of input).
+template <class In>
+constexpr uint64_t pipe_chunk() { return (32ull << 20) / sizeof(In); }
+
+// Large host-pointer calls: the input is cut at character boundaries into
+// 32 MiB chunks (SURVEY.md 8(a) rules D/E, the same split as the sharder) and
+// streamed round-robin through three CUDA streams, so host->device copies,
+// kernels and device->host copies of neighbouring chunks overlap.
+// Per-chunk results combine exactly: written adds up, the first failing
+// chunk decides.  Pageable caller buffers go through pinned staging.
+template <class In, class Out, class Run, class Split>
+int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
+                             uint64_t out_cap_elems, vt_result* res, Run run, Split split,
+                             uint64_t out_mult) {
+  const uint64_t C = pipe_chunk<In>();
+  std::vector<uint64_t> st{0};
+  while (st.back() < n) {
+    const uint64_t cut = std::min(n, st.back() + C);
+    uint64_t s2 = cut < n ? split(in, n, cut) : n;
+    if (s2 <= st.back()) s2 = cut;  // no valid character spans the cut
+    st.push_back(s2);
+  }
+  const size_t K = st.size() - 1;
+  const size_t in_cap = (C + 16) * sizeof(In), out_cap = (C * out_mult + 32) * sizeof(Out);
+  for (int i = 0; i < HostCtx::kPipeBufs; i++) {
+    if (!c->ps[i]) {
+      VT_TRY(cudaStreamCreateWithFlags(&c->ps[i], cudaStreamNonBlocking));
+      VT_TRY(cudaEventCreateWithFlags(&c->pev[i], cudaEventDisableTiming));
+    }
+  }
+  if (c->pd_in_cap < in_cap || c->pd_out_cap < out_cap) {
+    for (int i = 0; i < HostCtx::kPipeBufs; i++) {
+      VT_TRY(cudaStreamSynchronize(c->ps[i]));
+      if (c->pd_in[i]) VT_TRY(cudaFree(c->pd_in[i]));
+      if (c->pd_out[i]) VT_TRY(cudaFree(c->pd_out[i]));
+      VT_TRY(cudaMalloc(&c->pd_in[i], in_cap));
+      VT_TRY(cudaMalloc(&c->pd_out[i], out_cap));
+    }
+    c->pd_in_cap = in_cap;
+    c->pd_out_cap = out_cap;
+  }
+  if (!c->pd_res) {
+    VT_TRY(cudaMalloc(&c->pd_res, HostCtx::kPipeBufs * sizeof(vt_result)));
+    VT_TRY(cudaMallocHost(&c->ph_res, HostCtx::kPipeBufs * sizeof(vt_result)));
+  }
+  const bool pin_in = host_pinned(in), pin_out = host_pinned(out);
+  if (!pin_in)
+    for (int i = 0; i < HostCtx::kPipeBufs; i++) {
+      size_t cap = c->ph_in_cap;
+      VT_TRY(ensure_pinned(c->ph_in[i], cap, in_cap));
+      if (i == HostCtx::kPipeBufs - 1) c->ph_in_cap = cap;
+    }
+  if (!pin_out)
+    for (int i = 0; i < HostCtx::kPipeBufs; i++) {
+      size_t cap = c->ph_out_cap;
+      VT_TRY(ensure_pinned(c->ph_out[i], cap, out_cap));
+      if (i == HostCtx::kPipeBufs - 1) c->ph_out_cap = cap;
+    }
+  auto issue = [&](size_t k) -> int {
+    const int b = (int)(k % HostCtx::kPipeBufs);
+    cudaStream_t s = c->ps[b];
+    const uint64_t len = st[k + 1] - st[k];
+    const In* src = in + st[k];
+    if (!pin_in) {
+      // the staging buffer was last read by chunk k-3's copy, which finished
+      // before its result was read
+      std::memcpy(c->ph_in[b], src, len * sizeof(In));
+      src = reinterpret_cast<const In*>(c->ph_in[b]);
+    }
+    VT_TRY(cudaMemcpyAsync(c->pd_in[b], src, len * sizeof(In), cudaMemcpyHostToDevice, s));
+    VT_TRY(run(reinterpret_cast<const In*>(c->pd_in[b]), len, reinterpret_cast<Out*>(c->pd_out[b]),
+               c->pd_res + b, s));
+    VT_TRY(cudaMemcpyAsync(c->ph_res + b, c->pd_res + b, sizeof(vt_result),
+                           cudaMemcpyDeviceToHost, s));
+    VT_TRY(cudaEventRecord(c->pev[b], s));
+    return 0;
+  };
+  for (size_t k = 0; k < K && k < (size_t)HostCtx::kPipeBufs; k++) VT_TRY(issue(k));
+  uint64_t written = 0;
+  res->error_at = -1;
+  res->consumed = n;
+  int rc = 0;
+  for (size_t k = 0; k < K; k++) {
+    const int b = (int)(k % HostCtx::kPipeBufs);
+    VT_TRY(cudaEventSynchronize(c->pev[b]));
+    const vt_result r = c->ph_res[b];
+    if (written + r.written > out_cap_elems) return VT_E_ARG;
+    if (r.written) {
+      if (pin_out) {
+        VT_TRY(cudaMemcpyAsync(out + written, c->pd_out[b], r.written * sizeof(Out),
+                               cudaMemcpyDeviceToHost, c->ps[b]));
+      } else {
+        VT_TRY(cudaMemcpyAsync(c->ph_out[b], c->pd_out[b], r.written * sizeof(Out),
+                               cudaMemcpyDeviceToHost, c->ps[b]));
+        VT_TRY(cudaStreamSynchronize(c->ps[b]));
+        std::memcpy(out + written, c->ph_out[b], r.written * sizeof(Out));
+      }
+    }
+    written += r.written;
+    if (r.error_at >= 0) {
+      res->error_at = (int64_t)st[k] + r.error_at;
+      res->consumed = (uint64_t)res->error_at;
+      break;
+    }
+    if (k + HostCtx::kPipeBufs < K) {
+      rc = issue(k + HostCtx::kPipeBufs);
+      if (rc) break;
+    }
+  }
+  for (int i = 0; i < HostCtx::kPipeBufs; i++) VT_TRY(cudaStreamSynchronize(c->ps[i]));
+  res->written = written;
+  return rc;
+}
+
 template <class In, class Out, class Run>
 int host_transcode(const In* in, uint64_t n, Out* out, uint64_t out_cap_elems, vt_result* res,
                    Run run) {
@@ -302,20 +448,19 @@ int host_transcode(const In* in, uint64_t n, Out* out, uint64_t out_cap_elems, v
     if (res->written) std::memcpy(out, c->h_out, res->written * sizeof(Out));
     return 0;
   }
-  VT_TRY(ensure_dev(c->d_in, c->d_in_cap, in_bytes, c->stream));
-  VT_TRY(ensure_dev(c->d_out, c->d_out_cap, out_cap_elems * sizeof(Out) + 16, c->stream));
-  VT_TRY(cudaMemcpyAsync(c->d_in, in, in_bytes, cudaMemcpyHostToDevice, c->stream));
-  VT_TRY(run(reinterpret_cast<const In*>(c->d_in), n, reinterpret_cast<Out*>(c->d_out), c->d_res,
-             c->stream));
-  VT_TRY(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(vt_result), cudaMemcpyDeviceToHost, c->stream));
-  VT_TRY(cudaStreamSynchronize(c->stream));
-  *res = *c->h_res;
-  if (res->written > out_cap_elems) return VT_E_ARG;
-  if (res->written)
-    VT_TRY(cudaMemcpyAsync(out, c->d_out, res->written * sizeof(Out), cudaMemcpyDeviceToHost,
-                           c->stream));
-  VT_TRY(cudaStreamSynchronize(c->stream));
-  return 0;
+  if (sizeof(In) == 1)
+    return host_transcode_pipelined(c, in, n, out, out_cap_elems, res, run,
+                                    [](const In* p, uint64_t m, uint64_t cut) {
+                                      return vt_split_point_utf8(
+                                          reinterpret_cast<const uint8_t*>(p), m, cut);
+                                    },
+                                    1);
+  return host_transcode_pipelined(c, in, n, out, out_cap_elems, res, run,
+                                  [](const In* p, uint64_t m, uint64_t cut) {
+                                    return vt_split_point_utf16(
+                                        reinterpret_cast<const uint16_t*>(p), m, cut);
+                                  },
+                                  3);
 }
 
 template <class In, class Run>

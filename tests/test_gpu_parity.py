@@ -374,3 +374,34 @@ def test_reference_acceptance_harness_on_gpu():
     lines = {int(l.split(":")[0].split()[1]): l for l in p.stdout.splitlines() if l.startswith("criterion")}
     for c in (1, 2, 3, 4, 5, 6, 7, 10):
         assert "PASS" in lines[c], lines.get(c)
+
+
+def test_host_pipeline_multi_chunk(oracle, torch):
+    """Host-pointer calls above one 64 MiB pipeline chunk: chunk cuts at
+    character boundaries, results combined exactly, pageable and pinned
+    buffers, an error after the first cut."""
+    d_in, n, _ = vt.generate(5, 150 << 20)
+    host = d_in[:n].cpu().numpy()
+    for err in (None, (64 << 20) + 5, (128 << 20) + 1):
+        data = host.copy()
+        if err is not None:
+            data[err] = 0xFF
+        want_out, want = oracle.utf8_to_utf16(data, threads=_threads())
+        out, r = vt.utf8_to_utf16(data)  # pageable
+        assert _same(r, want) and np.array_equal(out, want_out), err
+        pin = torch.from_numpy(data).pin_memory()
+        import ctypes
+        o = torch.empty(len(data) + 8, dtype=torch.int16).pin_memory()
+        cr = vt._CRes()
+        assert vt.lib().vt_host_utf8_to_utf16(pin.data_ptr(), len(data), o.data_ptr(), ctypes.byref(cr)) == 0
+        assert (cr.consumed, cr.written, -1 if want.error_at is None else want.error_at) == \
+            (want.consumed, want.written, cr.error_at)
+        assert np.array_equal(o[: cr.written].numpy().view(np.uint16), want_out)
+    u16 = np.frombuffer(host.tobytes().decode("utf-8").encode("utf-16-le"), dtype=np.uint16).copy()
+    for err in (None, (32 << 20) + 3):
+        u = u16.copy()
+        if err is not None:
+            u[err] = 0xDC00
+        w8, w = oracle.utf16_to_utf8(u, threads=_threads())
+        o8, r8 = vt.utf16_to_utf8(u)
+        assert _same(r8, w) and np.array_equal(o8, w8), err
