@@ -58,6 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     nv = nvcc()
     common = ["-O3", "-std=c++20", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+    common += os.environ.get("VT_NVCC_EXTRA", "").split()
     cmds = []
     objs = []
     for src in CU_SOURCES:

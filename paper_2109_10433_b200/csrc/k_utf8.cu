@@ -31,7 +31,10 @@
 namespace vt {
 
 constexpr int K8_THREADS = kComputeThreads;
-constexpr int K8_WPT = 16;                      // words per thread
+#ifndef VT_K8_WPT
+#define VT_K8_WPT 16
+#endif
+constexpr int K8_WPT = VT_K8_WPT;               // words per thread
 constexpr int K8_BPT = 4 * K8_WPT;              // bytes per thread
 constexpr int K8_TILE = K8_THREADS * K8_BPT;    // bytes per tile
 constexpr unsigned kNone = 0xFFFFFFFFu;
@@ -139,18 +142,6 @@ __device__ __forceinline__ uint32_t susp_lanes(uint32_t x) {
   const uint32_t y = x & 0x1E1E1E1Eu;
   const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
   return z3 | z2;
-}
-
-// Interior load of a thread's window (16-byte vector loads + halo words).
-__device__ __forceinline__ void load_interior(const uint8_t* p, Words& W) {
-  const uint4* q = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-  for (int r = 0; r < 4; r++) {
-    const uint4 v = __ldg(q + r);
-    W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y; W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
-  }
-  W.w[0] = __ldg(reinterpret_cast<const uint32_t*>(p - 4));
-  W.w[K8_WPT + 1] = __ldg(reinterpret_cast<const uint32_t*>(p + K8_BPT));
 }
 
 // Exact range check of the leads flagged in m (bit 7 of each lane) of word x,
@@ -346,7 +337,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   if (interior) {
     const uint4* p = reinterpret_cast<const uint4*>(a.base + tc.v0);
 #pragma unroll
-    for (int r = 0; r < 4; r++) {
+    for (int r = 0; r < K8_WPT / 4; r++) {
       const uint4 v = __ldg(p + r);
       tc.W.w[1 + 4 * r] = v.x; tc.W.w[2 + 4 * r] = v.y;
       tc.W.w[3 + 4 * r] = v.z; tc.W.w[4 + 4 * r] = v.w;
@@ -441,7 +432,10 @@ __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Arg
   validate_body<Utf8Codec>(a);
 }
 
-__global__ void __launch_bounds__(kPipeBlock, 3) utf8_transcode_kernel(U8Args a) {
+#ifndef VT_K8_MINB
+#define VT_K8_MINB 3
+#endif
+__global__ void __launch_bounds__(kPipeBlock, VT_K8_MINB) utf8_transcode_kernel(U8Args a) {
   extern __shared__ __align__(16) uint8_t k8_dyn_smem[];
   transcode_body<Utf8Codec>(a, *reinterpret_cast<PipeSmem<Utf8Codec>*>(k8_dyn_smem));
 }

@@ -729,6 +729,17 @@ int vt_device_count(void) {
 
 uint64_t vt_launch_count(void) { return g_launches.load(); }
 
+// Debug: the 5 probe counters of the control block of (current device, stream).
+int vt_debug_probe(vt_stream stream, uint64_t* out5) {
+  int dev;
+  VT_TRY(current_device(dev));
+  Scratch* sc = scratch_for(dev, (cudaStream_t)stream);
+  if (!sc->ctl) return VT_E_ARG;
+  VT_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  VT_TRY(cudaMemcpy(out5, sc->ctl->pad, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 const char* vt_build_info(void) {
   return "libvtrans_gpu sm_100a (nvcc " VT_STR(__CUDACC_VER_MAJOR__) "." VT_STR(
       __CUDACC_VER_MINOR__) ")";

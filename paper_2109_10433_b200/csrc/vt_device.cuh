@@ -87,42 +87,51 @@ __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p
 // Warp-cooperative decoupled look-back for tile `tile` (> 0), executed by one
 // full warp.  Returns the exclusive prefix, or ~0ull when the tile became
 // irrelevant (a tile before it reported an error, so its output is never read).
-// Looks at 32 predecessors per step: lane i inspects tile (base - i).
+// Lane i inspects tile base - i (newest first).  When a step finds an inclusive
+// prefix, the warp also publishes the inclusive prefixes of the aggregate-only
+// tiles it summed on the way ("helping"), so the prefix frontier keeps up with
+// the tiles in flight and later look-backs stay one step deep.
 __device__ __forceinline__ unsigned long long lookback(unsigned long long* status, unsigned epoch,
                                                       unsigned tile, const Ctl* ctl,
                                                       unsigned long long tile_bytes,
                                                       unsigned long long head) {
   const unsigned lane = threadIdx.x & 31;
+  const unsigned ep = epoch & 0x3FFF;
   unsigned long long excl = 0;
-  long long base = (long long)tile - 1;
+  long long base = (long long)tile - 1;  // newest predecessor not yet summed
   unsigned spins = 0;
   while (true) {
     const long long idx = base - (long long)lane;
-    unsigned long long s = 0;
-    bool ready = true;
-    if (idx >= 0) {
-      s = load_status(&status[idx]);
-      ready = ((s >> 62) != 0) && (((s >> 48) & 0x3FFF) == (epoch & 0x3FFF));
-    }
-    // lanes past tile 0 behave like an inclusive prefix of 0
-    const bool is_pre = idx < 0 || (ready && (s >> 62) == 2);
-    const unsigned ready_mask = __ballot_sync(0xffffffffu, ready || idx < 0);
-    const unsigned pre_mask = __ballot_sync(0xffffffffu, is_pre);
-    // the contiguous run of ready lanes starting at lane 0
-    const unsigned run = ready_mask == 0xffffffffu ? 32u : (unsigned)__ffs(~ready_mask) - 1u;
-    const unsigned pre_in_run = pre_mask & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
-    if (pre_in_run) {
-      const unsigned stop = (unsigned)__ffs(pre_in_run) - 1u;  // nearest inclusive prefix
-      unsigned long long v = (lane <= stop && idx >= 0) ? (s & kValMask) : 0ull;
+    const unsigned long long s = idx >= 0 ? load_status(&status[idx]) : 0ull;
+    const bool ready = idx < 0 || (((s >> 62) != 0) && (((s >> 48) & 0x3FFF) == ep));
+    const bool is_pre = idx < 0 || (ready && (s >> 62) == 2);  // before tile 0: prefix 0
+    const unsigned long long v = idx < 0 ? 0ull : (s & kValMask);
+    const unsigned rm = __ballot_sync(0xffffffffu, ready);
+    const unsigned pm = __ballot_sync(0xffffffffu, is_pre);
+    const unsigned run = rm == 0xffffffffu ? 32u : (unsigned)__ffs(~rm) - 1u;
+    const unsigned pre_in = pm & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
+    if (pre_in) {
+      const unsigned stop = (unsigned)__ffs(pre_in) - 1u;  // nearest inclusive prefix
+      // suffix sums over lanes [lane, stop): inclusive prefix of tile base - lane
+      unsigned long long x = lane < stop ? v : 0ull;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      return excl + v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_down_sync(0xffffffffu, x, o);
+        if (lane + o < 32) x += y;
+      }
+      const unsigned long long pval = __shfl_sync(0xffffffffu, v, stop);
+      if (lane < stop) store_status(&status[idx], pack_status(kFlagPre, epoch, pval + x));
+      // this tile's exclusive prefix: everything newer than the prefix tile
+      return excl + __shfl_sync(0xffffffffu, x, 0) + pval;
     }
+#ifdef VT_PROBE
+    if (lane == 0) atomicAdd(const_cast<unsigned long long*>(&ctl->pad[4]), run > 0 ? (1ull << 32) : 1ull);
+#endif
     if (run > 0) {
-      unsigned long long v = (lane < run) ? (s & kValMask) : 0ull;
+      unsigned long long t = lane < run ? v : 0ull;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      excl += v;
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      excl += t;
       base -= (long long)run;
       continue;
     }

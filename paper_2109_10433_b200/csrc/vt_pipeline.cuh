@@ -27,7 +27,7 @@ namespace vt {
 
 constexpr int kComputeThreads = 256;
 constexpr int kPipeBlock = kComputeThreads + 32;
-constexpr int BAR_COMPUTE = 1, BAR_AGG = 2, BAR_EXCL = 3;
+constexpr int BAR_COMPUTE = 1;
 constexpr unsigned kSentinel = 0xFFFFFFFFu;
 using ComputeSync = SyncNamed<BAR_COMPUTE, kComputeThreads>;
 
@@ -97,8 +97,11 @@ struct PipeSmem {
   unsigned scan[kComputeThreads / 32];
   unsigned red[kComputeThreads / 32];
   unsigned tile;
-  unsigned agg_tile[2], agg[2];
-  unsigned long long excl[2];
+  // hand-off between the compute warps and the look-back warp (2-slot rings,
+  // sequence numbers polled by one thread; no barrier couples the two roles)
+  volatile unsigned agg_tile[2], agg[2];
+  volatile unsigned long long excl[2];
+  volatile unsigned seq_agg, seq_excl;
 };
 
 template <class C>
@@ -109,28 +112,52 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
            kComputeThreads);
 }
 
+__device__ __forceinline__ void spin_until(volatile unsigned* seq, unsigned target) {
+  unsigned n = 0;
+  while (*seq < target) {
+    if (++n > 4) __nanosleep(20);
+  }
+}
+
 template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
+  if (threadIdx.x == 0) {
+    sm.seq_agg = 0;
+    sm.seq_excl = 0;
+  }
+  __syncthreads();
   if (threadIdx.x >= kComputeThreads) {
-    // look-back warp
+    // look-back warp: publishes each tile's aggregate as soon as the compute
+    // warps have counted it, resolves its offset, hands the offset back
     const bool leader = threadIdx.x == kComputeThreads;
     for (unsigned j = 0;; j++) {
-      bar_sync(BAR_AGG, kPipeBlock);
+      if (leader) spin_until(&sm.seq_agg, j + 1);
+      __syncwarp();
       const unsigned tile = sm.agg_tile[j & 1];
       if (tile == kSentinel) break;
       const unsigned agg = sm.agg[j & 1];
       unsigned long long excl = 0;
-      if (tile == 0) {
-        if (leader) store_status(&a.status[0], pack_status(kFlagPre, a.epoch, agg));
-      } else {
-        if (leader) store_status(&a.status[tile], pack_status(kFlagAgg, a.epoch, agg));
+      if (tile != 0) {
+        // (the compute warps already published this tile's aggregate)
+#ifdef VT_PROBE
+        const long long t0 = clock64();
+#endif
         excl = lookback(a.status, a.epoch, tile, a.ctl, C::kTileElems, a.head);
+#ifdef VT_PROBE
+        if (leader) {
+          atomicAdd(&a.ctl->pad[0], (unsigned long long)(clock64() - t0));
+          atomicAdd(&a.ctl->pad[1], 1ull);
+        }
+#endif
         if (leader && excl != ~0ull)
           store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
       }
-      if (leader) sm.excl[j & 1] = excl;
+      if (leader) {
+        sm.excl[j & 1] = excl;
+        __threadfence_block();
+        sm.seq_excl = j + 1;
+      }
       __syncwarp();
-      bar_arrive(BAR_EXCL, kPipeBlock);
     }
   } else {
     // compute warps
@@ -143,27 +170,46 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       typename C::TileCount tc;
       unsigned off, agg;
       C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
-      if (j > 0) {
-        // tile j-1: wait for its offset (resolved meanwhile), copy it out
-        bar_sync(BAR_EXCL, kPipeBlock);
-        copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
-      }
       if (threadIdx.x == 0) {
+        // publish the aggregate right away (tile 0: the inclusive prefix), so
+        // other CTAs' look-backs never wait on this CTA's look-back warp; then
+        // hand tile j to the look-back warp
+        store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
         sm.agg_tile[j & 1] = tile;
         sm.agg[j & 1] = agg;
+        __threadfence_block();
+        sm.seq_agg = j + 1;
       }
-      bar_arrive(BAR_AGG, kPipeBlock);
+      if (j > 0) {
+        // tile j-1: its offset was resolved meanwhile; copy it out
+        if (threadIdx.x == 0) {
+#ifdef VT_PROBE
+          const long long t0 = clock64();
+#endif
+          spin_until(&sm.seq_excl, j);
+#ifdef VT_PROBE
+          atomicAdd(&a.ctl->pad[2], (unsigned long long)(clock64() - t0));
+          atomicAdd(&a.ctl->pad[3], 1ull);
+#endif
+        }
+        ComputeSync::sync();
+        copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
+      }
       C::emit(a, tc, sm.out[j & 1], off);
       if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
       prev_agg = agg;
       j++;
     }
     if (j > 0) {
-      bar_sync(BAR_EXCL, kPipeBlock);
+      if (threadIdx.x == 0) spin_until(&sm.seq_excl, j);
+      ComputeSync::sync();
       copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
     }
-    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
-    bar_arrive(BAR_AGG, kPipeBlock);
+    if (threadIdx.x == 0) {
+      sm.agg_tile[j & 1] = kSentinel;
+      __threadfence_block();
+      sm.seq_agg = j + 1;
+    }
   }
   finalize_if_last(a, true, C::kTileElems);
 }
