@@ -79,6 +79,33 @@ int vt_host_validate_utf16(const uint16_t* in, uint64_t n, int64_t* first_err);
 int vt_host_count_utf8(const uint8_t* in, uint64_t n, int64_t* count);
 int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count);
 
+/* ---- UTF-16 big-endian and byte-order marks --------
+ * The reference converts big-endian UTF-16 with a separate byte-swap pass
+ * around its little-endian kernels (proj/src/harness.cpp:178-199); here the
+ * swap is fused into the kernels' loads (UTF-16BE input) and stores (UTF-16BE
+ * output).  Same results and contracts as the little-endian entry points. */
+int vt_utf8_to_utf16be_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
+                             vt_stream stream);
+int vt_utf16be_to_utf8_async(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res,
+                             vt_stream stream);
+int vt_validate_utf16be_async(const uint16_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream);
+int vt_host_utf8_to_utf16be(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res);
+int vt_host_utf16be_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, vt_result* res);
+int vt_host_validate_utf16be(const uint16_t* in, uint64_t n, int64_t* first_err);
+
+/* Whole-buffer transcode with BOM detection and endianness handling, the
+ * semantics of vtrans::harness::transcode_bytes (proj/include/vtrans/harness.hpp:
+ * 60-69, proj/src/harness.cpp:202-294).  Formats: 0 UTF-8, 1 UTF-16LE,
+ * 2 UTF-16BE; BOM policy: 0 keep, 1 strip, 2 add.  `out` needs
+ * 2n + 4 bytes (UTF-8 -> UTF-16), 3n/2 + 20 (UTF-16 -> UTF-8) or n + 4.
+ * *exit_code: 0 ok, 1 error (the reference's exit codes); *status:
+ * 0 ok, 1 BOM conflicts with the declared endianness, 2 odd byte count,
+ * 3 invalid UTF-8 at *error_at (bytes, after a stripped BOM), 4 invalid UTF-16
+ * at *error_at (units); bit 8 set: a UTF-8 BOM was stripped from the input. */
+int vt_host_transcode_bytes(const uint8_t* in, uint64_t n, int from, int to, int bom,
+                            uint8_t* out, uint64_t out_cap, uint64_t* out_len, int* exit_code,
+                            int* status, int64_t* error_at);
+
 /* ---- batched short strings ------------------------------------------------
  * `count` strings back to back in `d_data`; string i is
  * [d_offsets[i], d_offsets[i+1]).  Writes the first error index or -1. */

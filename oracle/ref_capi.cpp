@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "vtrans/codec_core.hpp"
+#include "vtrans/harness.hpp"
 #include "vtrans/utf16_to_utf8.hpp"
 #include "vtrans/utf8_to_utf16.hpp"
 #include "vtrans/validation.hpp"
@@ -185,6 +186,23 @@ uint64_t vtr_exhaustive_short_verdicts(uint8_t* verdict) {
     }
   }
   return k;
+}
+
+// vtrans::harness::transcode_bytes (proj/include/vtrans/harness.hpp:60-69).
+// Writes up to cap output bytes and the message (NUL-terminated, up to mcap).
+int vtr_transcode_bytes(const uint8_t* in, uint64_t n, int from, int to, int bom, uint8_t* out,
+                        uint64_t cap, uint64_t* out_len, char* msg, uint64_t mcap) {
+  using namespace vtrans::harness;
+  const Format f[3] = {Format::utf8, Format::utf16le, Format::utf16be};
+  const BomPolicy b[3] = {BomPolicy::keep, BomPolicy::strip, BomPolicy::add};
+  auto r = transcode_bytes(std::span<const uint8_t>(in, n), f[from], f[to], b[bom]);
+  const uint64_t k = std::min<uint64_t>(cap, r.output.size());
+  std::copy(r.output.begin(), r.output.begin() + k, out);
+  *out_len = r.output.size();
+  const uint64_t m = std::min<uint64_t>(mcap - 1, r.message.size());
+  std::copy(r.message.begin(), r.message.begin() + m, msg);
+  msg[m] = 0;
+  return r.exit_code;
 }
 
 }  // extern "C"

@@ -87,6 +87,15 @@ def lib():
         "vt_host_count_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
         "vt_host_count_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
         "vt_validate_utf8_batch": (C.c_int, [_vp, _vp, C.c_uint64, _vp, _vp]),
+        "vt_utf8_to_utf16be_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_utf16be_to_utf8_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_validate_utf16be_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+        "vt_host_utf8_to_utf16be": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes)]),
+        "vt_host_utf16be_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes)]),
+        "vt_host_validate_utf16be": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_host_transcode_bytes": (C.c_int, [_vp, C.c_uint64, C.c_int, C.c_int, C.c_int, _vp, C.c_uint64,
+                                              C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                              C.POINTER(C.c_int64)]),
         "vt_exhaustive_short_verdicts": (C.c_int, [_vp, _vp]),
         "vt_sharded_utf8_to_utf16": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
         "vt_sharded_utf16_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
@@ -191,6 +200,57 @@ def count_utf16(units) -> Optional[int]:
     c = C.c_int64()
     _check(lib().vt_host_count_utf16(_ptr(a), len(a), C.byref(c)), "count_utf16")
     return None if c.value < 0 else int(c.value)
+
+
+# ---- UTF-16 big-endian and byte-order marks --------------------------------------
+
+def utf8_to_utf16be(data):
+    """UTF-8 -> UTF-16BE units (as host-order uint16 values holding the
+    big-endian byte pairs, i.e. ``out.tobytes()`` is the UTF-16BE byte stream)."""
+    a = _bytes_view(data)
+    out = np.empty(len(a) + 8, dtype=np.uint16)
+    r = _CRes()
+    _check(lib().vt_host_utf8_to_utf16be(_ptr(a), len(a), out.ctypes.data, C.byref(r)), "utf8_to_utf16be")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def utf16be_to_utf8(units):
+    """``units`` holds UTF-16BE byte pairs (e.g. np.frombuffer(be_bytes, np.uint16))."""
+    a = _units_view(units)
+    out = np.empty(3 * len(a) + 16, dtype=np.uint8)
+    r = _CRes()
+    _check(lib().vt_host_utf16be_to_utf8(_ptr(a), len(a), out.ctypes.data, C.byref(r)), "utf16be_to_utf8")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+FORMATS = {"utf8": 0, "utf16le": 1, "utf16be": 2}
+BOM_POLICIES = {"keep": 0, "strip": 1, "add": 2}
+
+
+def transcode_bytes(data, from_format: str, to_format: str, bom: str = "strip"):
+    """harness::transcode_bytes (proj/include/vtrans/harness.hpp:60-69): returns
+    (exit_code, message, output bytes) with the reference's codes and messages."""
+    a = _bytes_view(data)
+    f, t = FORMATS[from_format], FORMATS[to_format]
+    cap = 2 * len(a) + 4 if (f == 0 and t != 0) else (3 * (len(a) // 2) + 20 if (f != 0 and t == 0) else len(a) + 4)
+    out = np.empty(max(cap, 1), dtype=np.uint8)
+    n_out, code, status, err = C.c_uint64(), C.c_int(), C.c_int(), C.c_int64()
+    _check(lib().vt_host_transcode_bytes(_ptr(a), len(a), f, t, BOM_POLICIES[bom], out.ctypes.data, len(out),
+                                         C.byref(n_out), C.byref(code), C.byref(status), C.byref(err)),
+           "transcode_bytes")
+    st = status.value & 0xFF
+    msg = "warning: UTF-8 BOM stripped from input\n" if status.value & 0x100 else ""
+    if st == 1:
+        msg = "error: byte-order mark conflicts with declared endianness"
+    elif st == 2:
+        msg = "error: odd byte count for UTF-16 input"
+    elif st == 3:
+        msg = f"error: invalid UTF-8 at byte {err.value}"
+    elif st == 4:
+        msg = f"error: invalid UTF-16 at unit {err.value}"
+    return code.value, msg, bytes(out[: n_out.value]) if code.value == 0 else b""
 
 
 # ---- device-pointer API (torch tensors) --------------------------------------

@@ -9,6 +9,8 @@
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
+#include <algorithm>
+
 namespace vt {
 
 // First error index of bytes [p, p+n), or -1.
@@ -66,6 +68,22 @@ __global__ void exhaustive_short_kernel(uint8_t* verdicts) {
   }
   for (unsigned i = 0; i < len; i++) b[i] = (uint8_t)(v >> (8 * (len - 1 - i)));
   verdicts[k] = first_error_seq(b, len) < 0 ? 1 : 0;
+}
+
+// UTF-16LE <-> UTF-16BE: swap the two bytes of every unit (n units).
+__global__ void bswap16_kernel(const uint32_t* in, uint32_t* out, uint64_t nwords) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = prmt(in[i], 0, 0x2301);
+}
+
+int launch_bswap16(const uint16_t* in, uint16_t* out, uint64_t n, cudaStream_t s) {
+  if (n == 0) return 0;
+  // device buffers from cudaMalloc: 4-byte aligned; an odd tail unit is padded
+  const uint64_t nwords = (n + 1) / 2;
+  bswap16_kernel<<<(unsigned)std::min<uint64_t>((nwords + 255) / 256, 148 * 8), 256, 0, s>>>(
+      reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), nwords);
+  return (int)cudaGetLastError();
 }
 
 int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,

@@ -40,6 +40,7 @@ __device__ __forceinline__ uint32_t nz_hi6(uint32_t v) {
 struct Src16 {
   const uint16_t* base;
   unsigned long long head, n;
+  bool be;  // UTF-16BE input: bytes of each unit swapped on load
 };
 
 struct Words16 {
@@ -57,7 +58,11 @@ __device__ __noinline__ void load_masked16(Src16 a, long long v0, Words16& W) {
     uint32_t x = 0;
     for (int b = 0; b < 2; b++) {
       const long long p = v0 - 2 + 2 * k + b;
-      if (p >= lo && p < hi) x |= (uint32_t)a.base[p] << (16 * b);
+      if (p >= lo && p < hi) {
+        uint32_t u = a.base[p];
+        if (a.be) u = ((u & 0xFFu) << 8) | (u >> 8);
+        x |= u << (16 * b);
+      }
     }
     W.w[k] = x;
   }
@@ -178,14 +183,14 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
   return c;
 }
 
-template <bool kTranscode, int NT, class Sync>
+template <bool kTranscode, int NT, class Sync, bool kBE = false>
 __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, unsigned* red,
                                              unsigned* scan, TileCount16& tc, unsigned& off,
                                              unsigned& agg) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K16_TILE;
   tc.v0 = vt0 + (long long)K16_UPT * threadIdx.x;
-  const Src16 src{a.base, a.head, a.n};
+  const Src16 src{a.base, a.head, a.n, kBE};
   const bool interior =
       vt0 - 2 >= (long long)a.head && vt0 + K16_TILE + 2 <= (long long)(a.head + a.n);
   if (interior) {
@@ -202,6 +207,10 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
     if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 + K16_UPT));
     tc.W.w[0] = pw;
     tc.W.w[K16_WPT + 1] = nw;
+    if (kBE) {
+#pragma unroll
+      for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = prmt(tc.W.w[k], 0, 0x2301);
+    }
   } else {
     Words16 L;
     load_masked16(src, tc.v0, L);
@@ -284,6 +293,7 @@ __device__ __forceinline__ void emit_word16(uint32_t x, uint32_t nxw, uint32_t& 
   }
 }
 
+template <bool kBE>
 struct Utf16Codec {
   using Args = U16Args;
   using TileCount = TileCount16;
@@ -294,7 +304,7 @@ struct Utf16Codec {
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
                                                unsigned& agg) {
-    count_tile16<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg);
+    count_tile16<kTranscode, NT, Sync, kBE>(a, tile, red, scan, tc, off, agg);
   }
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
                                               unsigned off) {
@@ -303,33 +313,44 @@ struct Utf16Codec {
 #pragma unroll
       for (int k = 1; k <= K16_WPT; k++) emit_word16(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
-      generic_units(Src16{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off);
+      generic_units(Src16{a.base, a.head, a.n, kBE}, tc.v0, tc.lo, tc.lim, true, stage + off);
     }
   }
 };
 
+template <bool kBE>
 __global__ void __launch_bounds__(kComputeThreads, 4) utf16_validate_kernel(U16Args a) {
-  validate_body<Utf16Codec>(a);
+  validate_body<Utf16Codec<kBE>>(a);
 }
 
+// UTF-16LE (kBE = false) or UTF-16BE (kBE = true) -> UTF-8
+template <bool kBE>
 __global__ void __launch_bounds__(kPipeBlock, 3) utf16_transcode_kernel(U16Args a) {
   extern __shared__ __align__(16) uint8_t k16_dyn_smem[];
-  transcode_body<Utf16Codec>(a, *reinterpret_cast<PipeSmem<Utf16Codec>*>(k16_dyn_smem));
+  transcode_body<Utf16Codec<kBE>>(a, *reinterpret_cast<PipeSmem<Utf16Codec<kBE>>*>(k16_dyn_smem));
 }
 
 static int set_smem_attr16() {
-  return (int)cudaFuncSetAttribute(utf16_transcode_kernel,
+  int rc = (int)cudaFuncSetAttribute(utf16_transcode_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     sizeof(PipeSmem<Utf16Codec<false>>));
+  if (rc) return rc;
+  return (int)cudaFuncSetAttribute(utf16_transcode_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   sizeof(PipeSmem<Utf16Codec>));
+                                   sizeof(PipeSmem<Utf16Codec<true>>));
 }
 
-int launch_utf16(const U16Args& a, bool transcode, int grid, cudaStream_t s) {
+int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s) {
   static const int attr_rc = set_smem_attr16();
   if (attr_rc) return attr_rc;
-  if (transcode)
-    utf16_transcode_kernel<<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec>), s>>>(a);
+  if (mode == kModeTranscode)
+    utf16_transcode_kernel<false><<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec<false>>), s>>>(a);
+  else if (mode == kModeTranscodeBE)
+    utf16_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec<true>>), s>>>(a);
+  else if (mode == kModeValidateBE)
+    utf16_validate_kernel<true><<<grid, kComputeThreads, 0, s>>>(a);
   else
-    utf16_validate_kernel<<<grid, kComputeThreads, 0, s>>>(a);
+    utf16_validate_kernel<false><<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -337,10 +358,10 @@ int occupancy_utf16(bool transcode) {
   int n = 0;
   if (transcode) {
     if (set_smem_attr16()) return 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_transcode_kernel, kPipeBlock,
-                                                  sizeof(PipeSmem<Utf16Codec>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_transcode_kernel<false>, kPipeBlock,
+                                                  sizeof(PipeSmem<Utf16Codec<false>>));
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_validate_kernel, kComputeThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_validate_kernel<false>, kComputeThreads, 0);
   }
   return n;
 }

@@ -230,8 +230,13 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
 // ---- generic path (ends of the input, tiles with an error): rare, per byte --
 // Counts (units or characters) of the characters starting at positions
 // [lo, lim) of the thread's bytes; with `dst`, also writes their units.
+__device__ __forceinline__ uint16_t bswap16(unsigned u) {
+  return (uint16_t)(((u & 0xFFu) << 8) | ((u >> 8) & 0xFFu));
+}
+
 __device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
-                                               unsigned lim, bool units, uint16_t* dst) {
+                                               unsigned lim, bool units, uint16_t* dst,
+                                               bool be = false) {
   Words W;
   load_masked(a, v0, W);
   unsigned q = 0;
@@ -248,13 +253,14 @@ __device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
     if (!units) {
       q++;
     } else if (cp < 0x10000u) {
-      if (dst) dst[q] = (uint16_t)cp;
+      if (dst) dst[q] = be ? bswap16(cp) : (uint16_t)cp;
       q++;
     } else {
       const unsigned s = cp - 0x10000u;
       if (dst) {
-        dst[q] = (uint16_t)(0xD800u + (s >> 10));
-        dst[q + 1] = (uint16_t)(0xDC00u + (s & 0x3FFu));
+        const unsigned h = 0xD800u + (s >> 10), l = 0xDC00u + (s & 0x3FFu);
+        dst[q] = be ? bswap16(h) : (uint16_t)h;
+        dst[q + 1] = be ? bswap16(l) : (uint16_t)l;
       }
       q += 2;
     }
@@ -265,7 +271,7 @@ __device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
 // Branch-free decode of one word: lead-attributed byte planes of each
 // character's UTF-16 unit (BMP), plus, with kFour, the surrogate pair of
 // 4-byte characters.  Predicated 16-bit stores at the running offset q.
-template <bool kFour>
+template <bool kFour, bool kBE>
 __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
@@ -281,7 +287,8 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t lo = (c & ~mna) | (lom & mna);
   const uint32_t him = ((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3);
   const uint32_t hi = him & mna;
-  uint32_t u01 = prmt(lo, hi, 0x5140), u23 = prmt(lo, hi, 0x7362);
+  // units of lanes 0,1 and 2,3 (little-endian; UTF-16BE swaps the two bytes)
+  uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140), u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
   if (!kFour) {
     if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
     if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
@@ -294,11 +301,16 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
     const uint32_t m4 = prmt(four7, 0, 0xBA98);
     const uint32_t X = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
     const uint32_t c7 = c & 0x07070707u;
-    const uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
-    const uint32_t hs23 = prmt(X, c7, 0x7362) + 0xD7C0D7C0u;
+    uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
+    uint32_t hs23 = prmt(X, c7, 0x7362) + 0xD7C0D7C0u;
     const uint32_t lsl = ((n2 << 6) & 0xC0C0C0C0u) | (n3 & 0x3F3F3F3Fu);
     const uint32_t lsh = ((n2 >> 2) & 0x03030303u) | 0xDCDCDCDCu;
-    const uint32_t ls01 = prmt(lsl, lsh, 0x5140), ls23 = prmt(lsl, lsh, 0x7362);
+    const uint32_t ls01 = prmt(lsl, lsh, kBE ? 0x1504 : 0x5140);
+    const uint32_t ls23 = prmt(lsl, lsh, kBE ? 0x3726 : 0x7362);
+    if (kBE) {
+      hs01 = prmt(hs01, 0, 0x2301);
+      hs23 = prmt(hs23, 0, 0x2301);
+    }
     const uint32_t m4_01 = prmt(m4, 0, 0x1100), m4_23 = prmt(m4, 0, 0x3322);
     u01 = (u01 & ~m4_01) | (hs01 & m4_01);
     u23 = (u23 & ~m4_23) | (hs23 & m4_23);
@@ -394,22 +406,24 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
 }
 
 // ---- per-tile back half: decode into the staging buffer -----------------------
+template <bool kBE>
 __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
                                           unsigned off) {
   if (tc.simple) {
     uint32_t q = smem_addr(stage) + 2u * off;
     if (!tc.four) {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<false>(tc.W.w[k], tc.W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<false, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<true>(tc.W.w[k], tc.W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<true, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
     }
   } else {
-    generic_chars(Src{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off);
+    generic_chars(Src{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off, kBE);
   }
 }
 
+template <bool kBE>
 struct Utf8Codec {
   using Args = U8Args;
   using TileCount = vt::TileCount;
@@ -424,33 +438,41 @@ struct Utf8Codec {
   }
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
                                               unsigned off) {
-    emit_tile(a, tc, reinterpret_cast<uint16_t*>(stage), off);
+    emit_tile<kBE>(a, tc, reinterpret_cast<uint16_t*>(stage), off);
   }
 };
 
 __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Args a) {
-  validate_body<Utf8Codec>(a);
+  validate_body<Utf8Codec<false>>(a);
 }
 
 #ifndef VT_K8_MINB
 #define VT_K8_MINB 3
 #endif
+// UTF-8 -> UTF-16LE (kBE = false) or UTF-16BE (kBE = true)
+template <bool kBE>
 __global__ void __launch_bounds__(kPipeBlock, VT_K8_MINB) utf8_transcode_kernel(U8Args a) {
   extern __shared__ __align__(16) uint8_t k8_dyn_smem[];
-  transcode_body<Utf8Codec>(a, *reinterpret_cast<PipeSmem<Utf8Codec>*>(k8_dyn_smem));
+  transcode_body<Utf8Codec<kBE>>(a, *reinterpret_cast<PipeSmem<Utf8Codec<kBE>>*>(k8_dyn_smem));
 }
 
 static int set_smem_attr() {
-  return (int)cudaFuncSetAttribute(utf8_transcode_kernel,
+  int rc = (int)cudaFuncSetAttribute(utf8_transcode_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     sizeof(PipeSmem<Utf8Codec<false>>));
+  if (rc) return rc;
+  return (int)cudaFuncSetAttribute(utf8_transcode_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   sizeof(PipeSmem<Utf8Codec>));
+                                   sizeof(PipeSmem<Utf8Codec<true>>));
 }
 
-int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s) {
+int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s) {
   static const int attr_rc = set_smem_attr();
   if (attr_rc) return attr_rc;
-  if (transcode)
-    utf8_transcode_kernel<<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec>), s>>>(a);
+  if (mode == kModeTranscode)
+    utf8_transcode_kernel<false><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<false>>), s>>>(a);
+  else if (mode == kModeTranscodeBE)
+    utf8_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<true>>), s>>>(a);
   else
     utf8_validate_kernel<<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();
@@ -460,8 +482,8 @@ int occupancy_utf8(bool transcode) {
   int n = 0;
   if (transcode) {
     if (set_smem_attr()) return 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel, kPipeBlock,
-                                                  sizeof(PipeSmem<Utf8Codec>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel<false>, kPipeBlock,
+                                                  sizeof(PipeSmem<Utf8Codec<false>>));
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel, kComputeThreads, 0);
   }

@@ -141,7 +141,8 @@ int grid_for(unsigned tiles, int occ, int sms) {
 
 // Enqueues one UTF-8 kernel; the caller holds sc.mu.
 int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint64_t n,
-                    uint16_t* d_out, vt_result* d_res, cudaStream_t s, bool transcode) {
+                    uint16_t* d_out, vt_result* d_res, cudaStream_t s, int mode) {
+  const bool transcode = mode != vt::kModeValidate;
   if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
   vt::U8Args a;
   const uintptr_t p = (uintptr_t)d_in;
@@ -161,11 +162,12 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
   a.res = d_res;
   const int grid = grid_for(a.ntiles, di.occ_u8[transcode], di.sms);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return vt::launch_utf8(a, transcode, grid, s);
+  return vt::launch_utf8(a, mode, grid, s);
 }
 
 int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, uint64_t n,
-                     uint8_t* d_out, vt_result* d_res, cudaStream_t s, bool transcode) {
+                     uint8_t* d_out, vt_result* d_res, cudaStream_t s, int mode) {
+  const bool transcode = mode == vt::kModeTranscode || mode == vt::kModeTranscodeBE;
   if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
   if (((uintptr_t)d_in & 1) != 0) return VT_E_ARG;
   vt::U16Args a;
@@ -181,7 +183,7 @@ int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, ui
   a.res = d_res;
   const int grid = grid_for(a.ntiles, di.occ_u16[transcode], di.sms);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return vt::launch_utf16(a, transcode, grid, s);
+  return vt::launch_utf16(a, mode, grid, s);
 }
 
 struct Target {
@@ -198,19 +200,19 @@ int target(cudaStream_t s, Target& t) {
 }
 
 int run_utf8(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res, cudaStream_t s,
-             bool transcode) {
+             int mode) {
   Target t;
   VT_TRY(target(s, t));
   std::lock_guard<std::mutex> lk(t.sc->mu);
-  return run_utf8_locked(t.sc, t.di, d_in, n, d_out, d_res, s, transcode);
+  return run_utf8_locked(t.sc, t.di, d_in, n, d_out, d_res, s, mode);
 }
 
 int run_utf16(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res, cudaStream_t s,
-              bool transcode) {
+              int mode) {
   Target t;
   VT_TRY(target(s, t));
   std::lock_guard<std::mutex> lk(t.sc->mu);
-  return run_utf16_locked(t.sc, t.di, d_in, n, d_out, d_res, s, transcode);
+  return run_utf16_locked(t.sc, t.di, d_in, n, d_out, d_res, s, mode);
 }
 
 // Enqueues through `enqueue(scratch, devinfo, d_res)` and returns the result to
@@ -495,27 +497,27 @@ extern "C" {
 
 int vt_utf8_to_utf16_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
                            vt_stream stream) {
-  return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, true);
+  return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscode);
 }
 
 int vt_utf16_to_utf8_async(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res,
                            vt_stream stream) {
-  return run_utf16(d_in, n, d_out, d_res, (cudaStream_t)stream, true);
+  return run_utf16(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscode);
 }
 
 int vt_validate_utf8_async(const uint8_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream) {
-  return run_utf8(d_in, n, nullptr, d_res, (cudaStream_t)stream, false);
+  return run_utf8(d_in, n, nullptr, d_res, (cudaStream_t)stream, vt::kModeValidate);
 }
 
 int vt_validate_utf16_async(const uint16_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream) {
-  return run_utf16(d_in, n, nullptr, d_res, (cudaStream_t)stream, false);
+  return run_utf16(d_in, n, nullptr, d_res, (cudaStream_t)stream, vt::kModeValidate);
 }
 
 int vt_utf8_to_utf16(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* h_res,
                      vt_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
-    return run_utf8_locked(sc, di, d_in, n, d_out, d, s, true);
+    return run_utf8_locked(sc, di, d_in, n, d_out, d, s, vt::kModeTranscode);
   });
 }
 
@@ -523,35 +525,35 @@ int vt_utf16_to_utf8(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result
                      vt_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
-    return run_utf16_locked(sc, di, d_in, n, d_out, d, s, true);
+    return run_utf16_locked(sc, di, d_in, n, d_out, d, s, vt::kModeTranscode);
   });
 }
 
 int vt_validate_utf8(const uint8_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
-    return run_utf8_locked(sc, di, d_in, n, nullptr, d, s, false);
+    return run_utf8_locked(sc, di, d_in, n, nullptr, d, s, vt::kModeValidate);
   });
 }
 
 int vt_validate_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
   cudaStream_t s = (cudaStream_t)stream;
   return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
-    return run_utf16_locked(sc, di, d_in, n, nullptr, d, s, false);
+    return run_utf16_locked(sc, di, d_in, n, nullptr, d, s, vt::kModeValidate);
   });
 }
 
 int vt_host_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res) {
   return host_transcode(in, n, out, n, res,
                         [](const uint8_t* i, uint64_t k, uint16_t* o, vt_result* r, cudaStream_t s) {
-                          return run_utf8(i, k, o, r, s, true);
+                          return run_utf8(i, k, o, r, s, vt::kModeTranscode);
                         });
 }
 
 int vt_host_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, vt_result* res) {
   return host_transcode(in, n, out, 3 * n + 16, res,
                         [](const uint16_t* i, uint64_t k, uint8_t* o, vt_result* r, cudaStream_t s) {
-                          return run_utf16(i, k, o, r, s, true);
+                          return run_utf16(i, k, o, r, s, vt::kModeTranscode);
                         });
 }
 
@@ -559,7 +561,7 @@ int vt_host_validate_utf8(const uint8_t* in, uint64_t n, int64_t* first_err) {
   if (!first_err) return VT_E_ARG;
   vt_result r;
   VT_TRY(host_validate(in, n, &r, [](const uint8_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
-    return run_utf8(i, k, nullptr, d, s, false);
+    return run_utf8(i, k, nullptr, d, s, vt::kModeValidate);
   }));
   *first_err = r.error_at;
   return 0;
@@ -569,7 +571,7 @@ int vt_host_validate_utf16(const uint16_t* in, uint64_t n, int64_t* first_err) {
   if (!first_err) return VT_E_ARG;
   vt_result r;
   VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
-    return run_utf16(i, k, nullptr, d, s, false);
+    return run_utf16(i, k, nullptr, d, s, vt::kModeValidate);
   }));
   *first_err = r.error_at;
   return 0;
@@ -579,7 +581,7 @@ int vt_host_count_utf8(const uint8_t* in, uint64_t n, int64_t* count) {
   if (!count) return VT_E_ARG;
   vt_result r;
   VT_TRY(host_validate(in, n, &r, [](const uint8_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
-    return run_utf8(i, k, nullptr, d, s, false);
+    return run_utf8(i, k, nullptr, d, s, vt::kModeValidate);
   }));
   *count = r.error_at < 0 ? (int64_t)r.written : -1;
   return 0;
@@ -589,9 +591,188 @@ int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count) {
   if (!count) return VT_E_ARG;
   vt_result r;
   VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
-    return run_utf16(i, k, nullptr, d, s, false);
+    return run_utf16(i, k, nullptr, d, s, vt::kModeValidate);
   }));
   *count = r.error_at < 0 ? (int64_t)r.written : -1;
+  return 0;
+}
+
+int vt_utf8_to_utf16be_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
+                             vt_stream stream) {
+  return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscodeBE);
+}
+
+int vt_utf16be_to_utf8_async(const uint16_t* d_in, uint64_t n, uint8_t* d_out, vt_result* d_res,
+                             vt_stream stream) {
+  return run_utf16(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscodeBE);
+}
+
+int vt_validate_utf16be_async(const uint16_t* d_in, uint64_t n, vt_result* d_res, vt_stream stream) {
+  return run_utf16(d_in, n, nullptr, d_res, (cudaStream_t)stream, vt::kModeValidateBE);
+}
+
+int vt_host_utf8_to_utf16be(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res) {
+  return host_transcode(in, n, out, n, res,
+                        [](const uint8_t* i, uint64_t k, uint16_t* o, vt_result* r, cudaStream_t s) {
+                          return run_utf8(i, k, o, r, s, vt::kModeTranscodeBE);
+                        });
+}
+
+int vt_host_utf16be_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, vt_result* res) {
+  return host_transcode(in, n, out, 3 * n + 16, res,
+                        [](const uint16_t* i, uint64_t k, uint8_t* o, vt_result* r, cudaStream_t s) {
+                          return run_utf16(i, k, o, r, s, vt::kModeTranscodeBE);
+                        });
+}
+
+int vt_host_validate_utf16be(const uint16_t* in, uint64_t n, int64_t* first_err) {
+  if (!first_err) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf16(i, k, nullptr, d, s, vt::kModeValidateBE);
+  }));
+  *first_err = r.error_at;
+  return 0;
+}
+
+// harness::transcode_bytes semantics over the GPU entry points (the host only
+// looks at the byte-order mark and moves bytes).
+int vt_host_transcode_bytes(const uint8_t* in, uint64_t n, int from, int to, int bom,
+                            uint8_t* out, uint64_t out_cap, uint64_t* out_len, int* exit_code,
+                            int* status, int64_t* error_at) {
+  if (!out_len || !exit_code || !status || !error_at || (n && !in) || from < 0 || from > 2 ||
+      to < 0 || to > 2 || bom < 0 || bom > 2)
+    return VT_E_ARG;
+  *out_len = 0;
+  *exit_code = 0;
+  *status = 0;
+  *error_at = -1;
+  bool had_bom = false;
+  int warn = 0;
+  if (from == 0) {
+    if (n >= 3 && in[0] == 0xEF && in[1] == 0xBB && in[2] == 0xBF) {
+      had_bom = true;
+      in += 3;
+      n -= 3;
+      warn = 0x100;  // "warning: UTF-8 BOM stripped from input"
+    }
+  } else {
+    if (n >= 2) {
+      const bool le = in[0] == 0xFF && in[1] == 0xFE, be = in[0] == 0xFE && in[1] == 0xFF;
+      if ((le && from == 2) || (be && from == 1)) {
+        *exit_code = 1;
+        *status = 1;
+        return 0;
+      }
+      if (le || be) {
+        had_bom = true;
+        in += 2;
+        n -= 2;
+      }
+    }
+    if (n % 2) {
+      *exit_code = 1;
+      *status = 2;
+      return 0;
+    }
+  }
+  const bool want_bom = bom == 2 || (bom == 0 && had_bom);
+  uint64_t pos = 0;
+  auto put_bom = [&]() {
+    if (!want_bom) return;
+    if (to == 0) {
+      out[0] = 0xEF; out[1] = 0xBB; out[2] = 0xBF;
+      pos = 3;
+    } else if (to == 1) {
+      out[0] = 0xFF; out[1] = 0xFE;
+      pos = 2;
+    } else {
+      out[0] = 0xFE; out[1] = 0xFF;
+      pos = 2;
+    }
+  };
+  vt_result r;
+  if (from == 0) {
+    if (to == 0) {
+      int64_t e;
+      VT_TRY(vt_host_validate_utf8(in, n, &e));
+      if (e >= 0) {
+        *exit_code = 1;
+        *status = 3 | warn;
+        *error_at = e;
+        return 0;
+      }
+      if (out_cap < n + 3) return VT_E_ARG;
+      put_bom();
+      if (n) std::memcpy(out + pos, in, n);
+      pos += n;
+    } else {
+      if (out_cap < 2 * n + 4) return VT_E_ARG;
+      put_bom();
+      VT_TRY(to == 1 ? vt_host_utf8_to_utf16(in, n, reinterpret_cast<uint16_t*>(out + pos), &r)
+                     : vt_host_utf8_to_utf16be(in, n, reinterpret_cast<uint16_t*>(out + pos), &r));
+      if (r.error_at >= 0) {
+        *exit_code = 1;
+        *status = 3 | warn;
+        *error_at = r.error_at;
+        *out_len = 0;
+        return 0;
+      }
+      pos += 2 * r.written;
+    }
+  } else {
+    const uint64_t units = n / 2;
+    // unit loads need 2-byte alignment: realign odd inputs through a copy
+    std::vector<uint16_t> tmp;
+    const uint16_t* u = reinterpret_cast<const uint16_t*>(in);
+    if (((uintptr_t)in & 1) != 0) {
+      tmp.resize(units);
+      if (units) std::memcpy(tmp.data(), in, n);
+      u = tmp.data();
+    }
+    if (to == 0) {
+      if (out_cap < 3 * units + 20) return VT_E_ARG;
+      put_bom();
+      VT_TRY(from == 1 ? vt_host_utf16_to_utf8(u, units, out + pos, &r)
+                       : vt_host_utf16be_to_utf8(u, units, out + pos, &r));
+      if (r.error_at >= 0) {
+        *exit_code = 1;
+        *status = 4;
+        *error_at = r.error_at;
+        return 0;
+      }
+      pos += r.written;
+    } else {
+      int64_t e;
+      VT_TRY(from == 1 ? vt_host_validate_utf16(u, units, &e) : vt_host_validate_utf16be(u, units, &e));
+      if (e >= 0) {
+        *exit_code = 1;
+        *status = 4;
+        *error_at = e;
+        return 0;
+      }
+      if (out_cap < n + 4) return VT_E_ARG;
+      put_bom();
+      if (from == to) {
+        if (n) std::memcpy(out + pos, u, n);
+      } else if (units) {
+        // endianness change: byte swap on the GPU
+        HostCtx* c;
+        VT_TRY(host_ctx(c));
+        VT_TRY(ensure_dev(c->d_in, c->d_in_cap, n + 4, c->stream));
+        VT_TRY(ensure_dev(c->d_out, c->d_out_cap, n + 4, c->stream));
+        VT_TRY(cudaMemcpyAsync(c->d_in, u, n, cudaMemcpyHostToDevice, c->stream));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        VT_TRY(vt::launch_bswap16(reinterpret_cast<const uint16_t*>(c->d_in),
+                                  reinterpret_cast<uint16_t*>(c->d_out), units, c->stream));
+        VT_TRY(cudaMemcpyAsync(out + pos, c->d_out, n, cudaMemcpyDeviceToHost, c->stream));
+        VT_TRY(cudaStreamSynchronize(c->stream));
+      }
+      pos += n;
+    }
+  }
+  *out_len = pos;
+  *status |= warn;
   return 0;
 }
 

@@ -40,17 +40,23 @@ struct U16Args {
   vt_result* res;
 };
 
-int launch_utf8(const U8Args& a, bool transcode, int grid, cudaStream_t s);
+// launch modes: validate/count, transcode to UTF-16LE / UTF-8, transcode to
+// UTF-16BE (UTF-8 side) / from UTF-16BE (UTF-16 side)
+constexpr int kModeValidate = 0, kModeTranscode = 1, kModeTranscodeBE = 2, kModeValidateBE = 3;
+
+int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf8(bool transcode);
 unsigned tiles_utf8(unsigned long long head, unsigned long long n);
 
-int launch_utf16(const U16Args& a, bool transcode, int grid, cudaStream_t s);
+int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf16(bool transcode);
 unsigned tiles_utf16(unsigned long long head, unsigned long long n);
 
 // Batched validation of many short strings (one warp per string).
 int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
                                int64_t* first_err, cudaStream_t s);
+// Byte swap of n UTF-16 units (device buffers, 4-byte aligned).
+int launch_bswap16(const uint16_t* in, uint16_t* out, uint64_t n, cudaStream_t s);
 // Every 1/2/3-byte input (acceptance C3 order), verdict per input.
 int launch_exhaustive_short(uint8_t* verdicts, cudaStream_t s);
 

@@ -195,8 +195,15 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         ComputeSync::sync();
         copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
       }
+#ifdef VT_EARLY_GRAB
+      unsigned next = 0;
+      if (threadIdx.x == 0) next = grab_tile(a, C::kTileElems);
+      C::emit(a, tc, sm.out[j & 1], off);
+      if (threadIdx.x == 0) sm.tile = next;
+#else
       C::emit(a, tc, sm.out[j & 1], off);
       if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
+#endif
       prev_agg = agg;
       j++;
     }

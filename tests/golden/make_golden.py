@@ -212,6 +212,27 @@ def main() -> None:
             u[int(rng.integers(0, len(u)))] ^= 1 << int(rng.integers(0, 16))
             add16("mutated units (cf. test_utf16_to_utf8.cpp:103-113)", u, full=False)
 
+    # --- harness::transcode_bytes: BOM / endianness policy (test_harness.cpp:87-141)
+    tb_cases = []
+    samples = [b"", "h\u00e9llo \u93e1 \U00010348".encode(), b"\xef\xbb\xbf" + "ab\u00e9".encode(),
+               b"\x41\xc2\xa3\xff\x42"]
+    u16s = ["hi \u93e1\U00024b62".encode("utf-16-le"), "hi \u93e1\U00024b62".encode("utf-16-be"),
+            b"\xff\xfe" + "x\u00e9".encode("utf-16-le"), b"\xfe\xff" + "x\u00e9".encode("utf-16-be"),
+            b"\xff\xfea\x00b", b"\x41\x00\x00\xdc", b"\x00\xd8\x41\x00"]
+    for data in samples:
+        for to in ("utf8", "utf16le", "utf16be"):
+            for bom in ("keep", "strip", "add"):
+                code, msg, out = ref.transcode_bytes(data, "utf8", to, bom)
+                tb_cases.append({"in": hx(data), "from": "utf8", "to": to, "bom": bom, "exit": code,
+                                 "msg": msg, "out": hx(out)})
+    for data in u16s:
+        for frm in ("utf16le", "utf16be"):
+            for to in ("utf8", "utf16le", "utf16be"):
+                for bom in ("keep", "strip", "add"):
+                    code, msg, out = ref.transcode_bytes(data, frm, to, bom)
+                    tb_cases.append({"in": hx(data), "from": frm, "to": to, "bom": bom, "exit": code,
+                                     "msg": msg, "out": hx(out)})
+
     verdicts = ref.exhaustive_short_verdicts()
     exhaustive = {
         "src": "acceptance.cpp:138-167 C3: validate_utf8 over every 1/2/3-byte input",
@@ -229,7 +250,8 @@ def main() -> None:
     with open(os.path.join(HERE, "utf16_to_utf8.json"), "w") as f:
         json.dump(u16_cases, f, separators=(",", ":"))
     with open(os.path.join(HERE, "misc.json"), "w") as f:
-        json.dump({"exhaustive_short": exhaustive, "encode": kats}, f, indent=1)
+        json.dump({"exhaustive_short": exhaustive, "encode": kats, "transcode_bytes": tb_cases}, f,
+                  indent=1)
     print(f"{len(u8_cases)} utf8 cases, {len(u16_cases)} utf16 cases, exhaustive valid={exhaustive['valid']}")
 
 

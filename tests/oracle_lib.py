@@ -169,6 +169,20 @@ class Reference:
         self._u16to8mt = L.fn("utf16_to_utf8_mt", None, _u16p, C.c_uint64, _u8p, C.c_int, C.POINTER(CRes))
         self._v8mt = L.fn("validate_utf8_mt", C.c_int, _u8p, C.c_uint64, C.c_int)
         self.native = bool(L.fn("native_backend", C.c_int)())
+        self._tb = L.fn("transcode_bytes", C.c_int, _u8p, C.c_uint64, C.c_int, C.c_int, C.c_int, _u8p,
+                        C.c_uint64, C.POINTER(C.c_uint64), C.c_char_p, C.c_uint64)
+
+    def transcode_bytes(self, data: bytes, from_format: str, to_format: str, bom: str = "strip"):
+        f = {"utf8": 0, "utf16le": 1, "utf16be": 2}
+        b = {"keep": 0, "strip": 1, "add": 2}
+        a = np.frombuffer(bytes(data), dtype=np.uint8) if data else np.zeros(1, np.uint8)
+        cap = 4 * len(data) + 64
+        out = np.zeros(cap, dtype=np.uint8)
+        n = C.c_uint64()
+        msg = C.create_string_buffer(512)
+        code = self._tb(_p8(a), len(data), f[from_format], f[to_format], b[bom], _p8(out), cap, C.byref(n),
+                        msg, 512)
+        return code, msg.value.decode(), bytes(out[: n.value]) if code == 0 else b""
 
     def utf8_to_utf16(self, data, validate=True, scalar=False, threads=1, out=None):
         a = np.ascontiguousarray(np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data, dtype=np.uint8)

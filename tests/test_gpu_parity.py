@@ -405,3 +405,45 @@ def test_host_pipeline_multi_chunk(oracle, torch):
         w8, w = oracle.utf16_to_utf8(u, threads=_threads())
         o8, r8 = vt.utf16_to_utf8(u)
         assert _same(r8, w) and np.array_equal(o8, w8), err
+
+
+def test_transcode_bytes_golden(golden):
+    """harness::transcode_bytes semantics (BOM detection / policy, endianness,
+    error codes and messages; proj/src/harness.cpp:202-294) on the GPU paths,
+    against the reference's own answers."""
+    for c in golden["misc"]["transcode_bytes"]:
+        code, msg, out = vt.transcode_bytes(bytes.fromhex(c["in"]), c["from"], c["to"], c["bom"])
+        assert (code, msg, out.hex()) == (c["exit"], c["msg"], c["out"]), c
+
+
+def test_utf16be_paths(oracle, torch):
+    """UTF-16BE output / input with the byte swap fused into the kernels, across
+    tiles and with errors, against the oracle plus an explicit swap."""
+    rng = np.random.default_rng(16)
+    for n in (0, 1, 5, 100, 20000, 300000):
+        text = _gen_text(rng, max(1, n), (40, 20, 25, 15)).encode()[:n]
+        for err in (None, len(text) // 2):
+            data = bytearray(text)
+            if err is not None and data:
+                data[err] = 0xC0
+            data = bytes(data)
+            want, wr = oracle.utf8_to_utf16(data)
+            out, r = vt.utf8_to_utf16be(data)
+            assert _same(r, wr) and np.array_equal(out, want.byteswap()), (n, err)
+            u = want.byteswap()  # UTF-16BE byte pairs
+            if err is None and len(u):
+                u = u.copy()
+                u[len(u) // 3] = 0x00DC  # lone low surrogate (big-endian bytes DC 00)
+            w8, w = oracle.utf16_to_utf8(u.byteswap())
+            o8, r8 = vt.utf16be_to_utf8(u)
+            assert _same(r8, w) and np.array_equal(o8, w8), (n, err)
+    # device-resident, multi-tile
+    d_in, n, _ = vt.generate(5, 8 << 20)
+    d16 = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+    res = torch.zeros(3, dtype=torch.int64, device="cuda")
+    assert vt.lib().vt_utf8_to_utf16be_async(d_in.data_ptr(), n, d16.data_ptr(), res.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream) == 0
+    r = vt.result_from_device(res)
+    want, wr = oracle.utf8_to_utf16(d_in[:n].cpu().numpy())
+    assert _same(r, wr)
+    assert np.array_equal(d16[: r.written].cpu().numpy().view(np.uint16), want.byteswap())
