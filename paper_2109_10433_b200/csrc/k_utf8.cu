@@ -157,18 +157,18 @@ __device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) 
 }
 
 // Leads whose value range depends on the next byte, as bit 7 of each lane:
-// C0 C1 (x & 0x1E == 0 among 2-byte leads), E0 ED (+ EE EF, harmless extras:
-// ((nibble + 3) & 0xC) == 0 among 3-byte leads), and 4-byte leads other than
-// F1..F3 (only F0 and F4 depend on the next byte; F5..FF are always invalid).
+// C0 C1, E0 ED (+ EE EF, harmless extras), F0 and F4..FF (F5..FF are always
+// invalid).  Per-lane unsigned compares x >= K on the low 7 bits (all leads
+// have bit 7 set; no carry crosses a lane): 1 AND + 5 ADD + 3 LOP3.
 __device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint32_t l3,
-                                                  uint32_t l4) {
-  const uint32_t ln = x & 0x0F0F0F0Fu;
-  const uint32_t t = ln + 0x03030303u;
-  const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
-  const uint32_t y = x & 0x1E1E1E1Eu;
-  const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
-  const uint32_t f_ok = (ln + 0x7F7F7F7Fu) & ~((ln & 0x0C0C0C0Cu) + 0x7C7C7C7Cu);  // ln in 1..3
-  return (z3 | z2 | (l4 & ~f_ok)) & H;
+                                                  uint32_t) {
+  const uint32_t x7 = x & 0x7F7F7F7Fu;
+  const uint32_t ge_c2 = x7 + 0x3E3E3E3Eu, ge_e1 = x7 + 0x1F1F1F1Fu;
+  const uint32_t ge_ed = x7 + 0x13131313u, ge_f1 = x7 + 0x0F0F0F0Fu;
+  const uint32_t ge_f4 = x7 + 0x0C0C0C0Cu;
+  const uint32_t f1 = ~ge_c2 | (l3 & ~ge_e1);  // C0 C1, E0
+  const uint32_t f2 = (ge_ed & ~ge_f1) | ge_f4;  // ED..F0, F4..FF
+  return (f1 | f2) & l2;
 }
 
 // Exact range check of the special leads of every word (only threads whose

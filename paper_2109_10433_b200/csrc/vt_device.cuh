@@ -146,48 +146,58 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 // (any alignment) with aligned 16-byte stores in the body.  Threads
 // 0..nthreads-1 participate.  `src` must have >= 16 readable bytes before and
 // >= 32 after.
-__device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
-                                         unsigned len, unsigned nthreads) {
-  if (len == 0) return;
-  const unsigned mis = (unsigned)((uintptr_t)dst & 15);  // chunk c <- src[16c - mis, +16)
+//
+// Chunk c of the destination needs source bytes [16c - mis, +16): words
+// WS..WS+4 of the two aligned 16-byte source chunks starting at 16(c-1) (+16
+// for mis == 0), then a byte funnel shift.  WS and the shift are the same for
+// every chunk, so the loop is instantiated per WS.
+template <int WS>
+__device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_t sbase,
+                                            unsigned mis, unsigned len, unsigned bs,
+                                            unsigned nthreads) {
   const unsigned nchunks = (mis + len + 15) >> 4;
-  uint8_t* dbase = dst - mis;
-  const uint32_t sbase = smem_addr(src);
-  // chunk c needs source bytes [16c - mis, +16): words ws..ws+4 of the two
-  // aligned 16-byte source chunks starting at 16(c-1) (+16 for mis == 0), then
-  // a byte funnel shift.  ws and the shift are the same for every chunk.
-  const unsigned rel = (16u - mis) & 15u;  // (16c - mis) mod 16
-  const unsigned ws = rel >> 2, bs = (rel & 3u) * 8u;
-  const int cbias = mis ? -1 : 0;
+  const unsigned end = mis + len;
+  // the first chunk may start before dst (mis != 0) and the last may end after
+  // it: those two go byte by byte, the rest with one 16-byte store
   for (unsigned c = threadIdx.x; c < nchunks; c += nthreads) {
-    const uint32_t a = sbase + (uint32_t)(16 * ((int)c + cbias));
-    uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+    const uint32_t a = sbase + 16u * c - (mis ? 16u : 0u);
+    uint32_t x[8];
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(a));
+                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a));
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3) : "r"(a + 16));
-    uint32_t w0, w1, w2, w3, w4;
-    if (ws == 0) { w0 = x0; w1 = x1; w2 = x2; w3 = x3; w4 = y0; }
-    else if (ws == 1) { w0 = x1; w1 = x2; w2 = x3; w3 = y0; w4 = y1; }
-    else if (ws == 2) { w0 = x2; w1 = x3; w2 = y0; w3 = y1; w4 = y2; }
-    else { w0 = x3; w1 = y0; w2 = y1; w3 = y2; w4 = y3; }
+                 : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(a + 16));
     uint4 v;
-    v.x = __funnelshift_r(w0, w1, bs);
-    v.y = __funnelshift_r(w1, w2, bs);
-    v.z = __funnelshift_r(w2, w3, bs);
-    v.w = __funnelshift_r(w3, w4, bs);
+    v.x = __funnelshift_r(x[WS], x[WS + 1], bs);
+    v.y = __funnelshift_r(x[WS + 1], x[WS + 2], bs);
+    v.z = __funnelshift_r(x[WS + 2], x[WS + 3], bs);
+    v.w = __funnelshift_r(x[WS + 3], x[WS + 4], bs);
     uint8_t* d = dbase + 16 * c;
-    const bool full = (c > 0 || mis == 0) && (16 * c + 16 <= mis + len);
-    if (full) {
+    if ((c > 0 || mis == 0) && 16 * c + 16 <= end) {
       *reinterpret_cast<uint4*>(d) = v;
     } else {
       const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int b = 0; b < 16; b++) {
         const unsigned pos = 16 * c + b;  // relative to dbase
-        if (pos >= mis && pos < mis + len) d[b] = (uint8_t)(vv[b >> 2] >> ((b & 3) * 8));
+        if (pos >= mis && pos < end) d[b] = (uint8_t)(vv[b >> 2] >> ((b & 3) * 8));
       }
     }
+  }
+}
+
+__device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
+                                         unsigned len, unsigned nthreads) {
+  if (len == 0) return;
+  const unsigned mis = (unsigned)((uintptr_t)dst & 15);
+  uint8_t* dbase = dst - mis;
+  const uint32_t sbase = smem_addr(src);
+  const unsigned rel = (16u - mis) & 15u;  // (16c - mis) mod 16
+  const unsigned bs = (rel & 3u) * 8u;
+  switch (rel >> 2) {
+    case 0: copy_out_ws<0>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 1: copy_out_ws<1>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 2: copy_out_ws<2>(dbase, sbase, mis, len, bs, nthreads); break;
+    default: copy_out_ws<3>(dbase, sbase, mis, len, bs, nthreads); break;
   }
 }
 

@@ -180,6 +180,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         __threadfence_block();
         sm.seq_agg = j + 1;
       }
+#ifdef VT_EMIT_FIRST
+      C::emit(a, tc, sm.out[j & 1], off);
+#endif
       if (j > 0) {
         // tile j-1: its offset was resolved meanwhile; copy it out
         if (threadIdx.x == 0) {
@@ -195,15 +198,10 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         ComputeSync::sync();
         copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
       }
-#ifdef VT_EARLY_GRAB
-      unsigned next = 0;
-      if (threadIdx.x == 0) next = grab_tile(a, C::kTileElems);
+#ifndef VT_EMIT_FIRST
       C::emit(a, tc, sm.out[j & 1], off);
-      if (threadIdx.x == 0) sm.tile = next;
-#else
-      C::emit(a, tc, sm.out[j & 1], off);
-      if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
 #endif
+      if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
       prev_agg = agg;
       j++;
     }
