@@ -97,11 +97,10 @@ struct PipeSmem {
   unsigned scan[kComputeThreads / 32];
   unsigned red[kComputeThreads / 32];
   unsigned tile;
-  // hand-off between the compute warps and the look-back warp (2-slot rings,
-  // sequence numbers polled by one thread; no barrier couples the two roles)
-  volatile unsigned agg_tile[2], agg[2];
-  volatile unsigned long long excl[2];
-  volatile unsigned seq_agg, seq_excl;
+  // hand-off between the compute warps and the look-back warp (2-slot rings
+  // indexed by tile parity, guarded by the named barriers below)
+  unsigned agg_tile[2], agg[2];
+  unsigned long long excl[2];
 };
 
 template <class C>
@@ -112,52 +111,44 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
            kComputeThreads);
 }
 
-__device__ __forceinline__ void spin_until(volatile unsigned* seq, unsigned target) {
-  unsigned n = 0;
-  while (*seq < target) {
-    if (++n > 4) __nanosleep(20);
-  }
-}
+// Hand-off barriers (all kPipeBlock threads): BAR_AGG + (j & 1) -- the compute
+// warps arrive once tile j's aggregate is in shared memory, the look-back warp
+// waits; BAR_EXCL + (j & 1) -- the look-back warp arrives once tile j's offset
+// is in shared memory, the compute warps wait.  bar.arrive orders the
+// producer's prior shared-memory writes before the consumer's bar.sync returns,
+// and a waiting warp issues nothing (no polling).  Two ids per direction keep
+// at most one pending instance per id: the compute warps can only arrive for
+// tile j+2 after waiting for tile j's offset, which the look-back warp
+// publishes only after its wait for tile j completed.
+constexpr int BAR_AGG = 2, BAR_EXCL = 4;
 
 template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
-  if (threadIdx.x == 0) {
-    sm.seq_agg = 0;
-    sm.seq_excl = 0;
-  }
-  __syncthreads();
   if (threadIdx.x >= kComputeThreads) {
-    // look-back warp: publishes each tile's aggregate as soon as the compute
-    // warps have counted it, resolves its offset, hands the offset back
-    const bool leader = threadIdx.x == kComputeThreads;
+    // look-back warp: resolves each tile's offset once the compute warps have
+    // counted it (and published its aggregate), hands the offset back
     for (unsigned j = 0;; j++) {
-      if (leader) spin_until(&sm.seq_agg, j + 1);
-      __syncwarp();
+      bar_sync(BAR_AGG + (j & 1), kPipeBlock);
       const unsigned tile = sm.agg_tile[j & 1];
       if (tile == kSentinel) break;
       const unsigned agg = sm.agg[j & 1];
       unsigned long long excl = 0;
       if (tile != 0) {
-        // (the compute warps already published this tile's aggregate)
 #ifdef VT_PROBE
         const long long t0 = clock64();
 #endif
         excl = lookback(a.status, a.epoch, tile, a.ctl, C::kTileElems, a.head);
 #ifdef VT_PROBE
-        if (leader) {
+        if (threadIdx.x == kComputeThreads) {
           atomicAdd(&a.ctl->pad[0], (unsigned long long)(clock64() - t0));
           atomicAdd(&a.ctl->pad[1], 1ull);
         }
 #endif
-        if (leader && excl != ~0ull)
+        if (threadIdx.x == kComputeThreads && excl != ~0ull)
           store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
       }
-      if (leader) {
-        sm.excl[j & 1] = excl;
-        __threadfence_block();
-        sm.seq_excl = j + 1;
-      }
-      __syncwarp();
+      if (threadIdx.x == kComputeThreads) sm.excl[j & 1] = excl;
+      bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
     }
   } else {
     // compute warps
@@ -172,48 +163,36 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
       if (threadIdx.x == 0) {
         // publish the aggregate right away (tile 0: the inclusive prefix), so
-        // other CTAs' look-backs never wait on this CTA's look-back warp; then
-        // hand tile j to the look-back warp
+        // other CTAs' look-backs never wait on this CTA's look-back warp
         store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
         sm.agg_tile[j & 1] = tile;
         sm.agg[j & 1] = agg;
-        __threadfence_block();
-        sm.seq_agg = j + 1;
       }
-#ifdef VT_EMIT_FIRST
-      C::emit(a, tc, sm.out[j & 1], off);
-#endif
+      bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
       if (j > 0) {
         // tile j-1: its offset was resolved meanwhile; copy it out
-        if (threadIdx.x == 0) {
 #ifdef VT_PROBE
-          const long long t0 = clock64();
+        const long long t0 = clock64();
 #endif
-          spin_until(&sm.seq_excl, j);
+        bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
 #ifdef VT_PROBE
+        if (threadIdx.x == 0) {
           atomicAdd(&a.ctl->pad[2], (unsigned long long)(clock64() - t0));
           atomicAdd(&a.ctl->pad[3], 1ull);
-#endif
         }
-        ComputeSync::sync();
+#endif
         copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
       }
-#ifndef VT_EMIT_FIRST
       C::emit(a, tc, sm.out[j & 1], off);
-#endif
       if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
       prev_agg = agg;
       j++;
     }
+    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
+    bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
     if (j > 0) {
-      if (threadIdx.x == 0) spin_until(&sm.seq_excl, j);
-      ComputeSync::sync();
+      bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
       copy_tile_out<C>(a, sm.out[(j - 1) & 1], sm.excl[(j - 1) & 1], prev_agg);
-    }
-    if (threadIdx.x == 0) {
-      sm.agg_tile[j & 1] = kSentinel;
-      __threadfence_block();
-      sm.seq_agg = j + 1;
     }
   }
   finalize_if_last(a, true, C::kTileElems);
