@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(kComputeThreads, 4) utf16_validate_kernel(U16A
 
 // UTF-16LE (kBE = false) or UTF-16BE (kBE = true) -> UTF-8
 template <bool kBE>
-__global__ void __launch_bounds__(kPipeBlock, 3) utf16_transcode_kernel(U16Args a) {
+#ifndef VT_K16_MINB
+#define VT_K16_MINB 4
+#endif
+__global__ void __launch_bounds__(kPipeBlock, VT_K16_MINB) utf16_transcode_kernel(U16Args a) {
   extern __shared__ __align__(16) uint8_t k16_dyn_smem[];
   transcode_body<Utf16Codec<kBE>>(a, *reinterpret_cast<PipeSmem<Utf16Codec<kBE>>*>(k16_dyn_smem));
 }

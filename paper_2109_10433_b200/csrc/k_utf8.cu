@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Arg
 }
 
 #ifndef VT_K8_MINB
-#define VT_K8_MINB 3
+#define VT_K8_MINB 4
 #endif
 // UTF-8 -> UTF-16LE (kBE = false) or UTF-16BE (kBE = true)
 template <bool kBE>
