@@ -228,11 +228,12 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
     if (er != kNone16) my_err = K16_UPT * threadIdx.x + er;
   }
   if (interior) {
-    static_assert(NT <= 256 && 4 * K16_TILE < (1 << 23), "packed scan fields");
+    constexpr int kErrShift = NT <= 256 ? 23 : 22;  // NT << kErrShift <= 2^31
+    static_assert(NT <= 512 && 4 * K16_TILE < (1 << kErrShift), "packed scan fields");
     tc.cnt = kTranscode ? c.bytes : c.chars;
     unsigned total;
-    off = block_excl_scan<NT, Sync, false>(my_err == kNone16 ? tc.cnt : (1u << 23), scan, total);
-    if ((total >> 23) == 0) {
+    off = block_excl_scan<NT, Sync, false>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), scan, total);
+    if ((total >> kErrShift) == 0) {
       tc.simple = true;
       agg = total;
       return;

@@ -133,17 +133,6 @@ struct ClassOut {
   bool four;       // a 4-byte lead (or F8..FF) in our bytes
 };
 
-// Suspicious leads of word x (bit 7 of each lane), see classify().
-__device__ __forceinline__ uint32_t susp_lanes(uint32_t x) {
-  const uint32_t x2 = x << 1;
-  const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
-  const uint32_t t = (x & 0x0F0F0F0Fu) + 0x03030303u;
-  const uint32_t z3 = ~((t & 0x0C0C0C0Cu) + 0x7C7C7C7Cu) & (l3 & ~l4);
-  const uint32_t y = x & 0x1E1E1E1Eu;
-  const uint32_t z2 = ~((y + 0x7F7F7F7Fu) | y) & (l2 & ~l3);
-  return z3 | z2;
-}
-
 // Exact range check of the leads flagged in m (bit 7 of each lane) of word x,
 // followed by word nx; true if one of them does not decode.
 __device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) {
@@ -156,19 +145,26 @@ __device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) 
   return bad;
 }
 
+// Continuation requirements of the lead planes of one word as a 64-bit sum:
+// lane i+1 (l2), i+2 (l3), i+3 (l4); the high half belongs to the next word.
+__device__ __forceinline__ unsigned long long need_plane(uint32_t l2, uint32_t l3, uint32_t l4) {
+  return (unsigned long long)l2 * 0x100u + (unsigned long long)l3 * 0x10000u +
+         (unsigned long long)l4 * 0x1000000u;
+}
+
 // Leads whose value range depends on the next byte, as bit 7 of each lane:
 // C0 C1, E0 ED (+ EE EF, harmless extras), F0 and F4..FF (F5..FF are always
 // invalid).  Per-lane unsigned compares x >= K on the low 7 bits (all leads
-// have bit 7 set; no carry crosses a lane): 1 AND + 5 ADD + 3 LOP3.
-__device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint32_t l3,
-                                                  uint32_t) {
+// have bit 7 set; no carry crosses a lane): the adds run on the FMA pipe
+// (VIADD), the three selections are single LOP3s.
+__device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint32_t l3) {
   const uint32_t x7 = x & 0x7F7F7F7Fu;
   const uint32_t ge_c2 = x7 + 0x3E3E3E3Eu, ge_e1 = x7 + 0x1F1F1F1Fu;
   const uint32_t ge_ed = x7 + 0x13131313u, ge_f1 = x7 + 0x0F0F0F0Fu;
   const uint32_t ge_f4 = x7 + 0x0C0C0C0Cu;
-  const uint32_t f1 = ~ge_c2 | (l3 & ~ge_e1);  // C0 C1, E0
-  const uint32_t f2 = (ge_ed & ~ge_f1) | ge_f4;  // ED..F0, F4..FF
-  return (f1 | f2) & l2;
+  const uint32_t g = lop3<0xBA>(ge_ed, ge_f1, ge_f4);  // (a & ~b) | c: ED..F0, F4..FF
+  const uint32_t h = lop3<0xA2>(g, ge_e1, l3);         // (a | ~b) & c: 3/4-byte specials
+  return lop3<0xBA>(l2, ge_c2, h);                     // (a & ~b) | c: + C0 C1
 }
 
 // Exact range check of the special leads of every word (only threads whose
@@ -180,8 +176,7 @@ __device__ __forceinline__ bool specials_fail(const Words& W) {
     const uint32_t x = W.w[k], x2 = x << 1;
     const uint32_t l2 = x & x2 & H;
     const uint32_t l3 = l2 & (x << 2);
-    const uint32_t l4 = l3 & (x << 3);
-    const uint32_t m = special_lanes(x, l2, l3, l4);
+    const uint32_t m = special_lanes(x, l2, l3) & H;
     if (m && lanes_fail(m, x, W.w[k + 1])) bad = true;
   }
   return bad;
@@ -189,33 +184,40 @@ __device__ __forceinline__ bool specials_fail(const Words& W) {
 
 // Phase A over the 16 own words (SWAR, branch-free): structure check,
 // special-lead flag, counts.
-__device__ __forceinline__ ClassOut classify(const Words& W) {
-  uint32_t p2, p3, p4;
+//
+// Structure: lane i must be a continuation exactly when a lead at i-1 (any
+// lead), i-2 (3/4-byte) or i-3 (4-byte) requires it.  The requirement planes
+// are summed, not ORed, as one 64-bit multiply-add chain per word (FMA pipe;
+// the high half spills into the next word): a lane required twice reads as not
+// required, but then the first lead inside the range of the earliest
+// overlapping lead is required exactly once while not being a continuation, so
+// "some lane differs" is unchanged.
+__device__ __forceinline__ ClassOut classify(const Words& W, const ShrK& K) {
+  uint32_t carry;  // requirement bits the previous word spills into this one
   {
     const uint32_t x = W.w[0], x2 = x << 1;
-    p2 = x & x2 & H;
-    p3 = p2 & (x << 2);
-    p4 = p3 & (x << 3);
+    const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
+    carry = (uint32_t)(need_plane(l2, l3, l4) >> 32);
   }
   uint32_t viol = 0, spec = 0, ccont = 0, cfour = 0;
 #pragma unroll
   for (int k = 1; k <= K8_WPT + 1; k++) {
-    const uint32_t x = W.w[k], x2 = x << 1, x8 = x << 3;
+    const uint32_t x = W.w[k], x2 = x << 1;
     const uint32_t c = x & ~x2 & H;
     const uint32_t l2 = x & x2 & H;
     const uint32_t l3 = l2 & (x << 2);
-    const uint32_t l4 = l3 & x8;
-    const uint32_t need = __funnelshift_l(p2, l2, 8) | __funnelshift_l(p3, l3, 16) |
-                          __funnelshift_l(p4, l4, 24);
+    const uint32_t l4 = l3 & (x << 3);
+    const unsigned long long t = need_plane(l2, l3, l4);
+    const uint32_t need = (uint32_t)t + carry;
+    carry = (uint32_t)(t >> 32);
     if (k <= K8_WPT) {
-      viol |= need ^ c;
-      spec |= special_lanes(x, l2, l3, l4);
-      ccont += c >> 7;
-      cfour += l4 >> 7;
+      viol = lop3<0xF6>(viol, need, c);  // a | (b ^ c)
+      spec |= special_lanes(x, l2, l3);
+      ccont = __umulhi(c, K.s7) + ccont;   // + continuation lanes (IMAD.HI)
+      cfour = __umulhi(l4, K.s7) + cfour;  // + 4-byte leads
     } else {
       viol |= (need ^ c) & 0x00808080u;  // next word: lanes that can blame our bytes
     }
-    p2 = l2; p3 = l3; p4 = l4;
   }
   ClassOut o;
   const unsigned nc = (ccont * 0x01010101u) >> 24, n4 = (cfour * 0x01010101u) >> 24;
@@ -369,7 +371,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
   tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
   const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
-  const ClassOut co = classify(tc.W);
+  const ClassOut co = classify(tc.W, a.k);
   tc.four = co.four;
   tc.lim = hi;
   unsigned my_err = kNone;
@@ -378,13 +380,14 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
   if (interior) {
-    // fast path: one scan; bits 23..31 count the threads that found an error
-    // (at most 256 << 23 = 2^31: no wrap; counts stay below 2^23)
-    static_assert(NT <= 256 && 2 * K8_TILE < (1 << 23), "packed scan fields");
+    // fast path: one scan; bits kErrShift..31 count the threads that found an error
+    // (NT << kErrShift <= 2^31: no wrap; counts stay below 2^kErrShift)
+    constexpr int kErrShift = NT <= 256 ? 23 : 22;  // NT << kErrShift <= 2^31
+    static_assert(NT <= 512 && 2 * K8_TILE < (1 << kErrShift), "packed scan fields");
     tc.cnt = kTranscode ? co.units : co.chars;
     unsigned total;
-    off = block_excl_scan<NT, Sync, false>(my_err == kNone ? tc.cnt : (1u << 23), scan, total);
-    if ((total >> 23) == 0) {
+    off = block_excl_scan<NT, Sync, false>(my_err == kNone ? tc.cnt : (1u << kErrShift), scan, total);
+    if ((total >> kErrShift) == 0) {
       tc.simple = true;
       agg = total;
       return;

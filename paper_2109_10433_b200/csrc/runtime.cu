@@ -155,6 +155,7 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
     return e ? (unsigned)std::strtoul(e, nullptr, 0) : 0u;
   }();
   a.dbg = dbg;
+  a.k = vt::shr_k();
   VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
   a.out = d_out;
   a.status = sc->status;
