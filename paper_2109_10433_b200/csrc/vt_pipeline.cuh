@@ -111,7 +111,7 @@ struct PipeSmem {
   unsigned tile;
   // hand-off between the compute warps and the look-back warp (2-slot rings
   // indexed by tile parity, guarded by the named barriers below)
-  unsigned agg_tile[2], agg[2];
+  unsigned lb_tile[2], agg[2];
   unsigned long long excl[2];
 };
 
@@ -123,27 +123,31 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
            kComputeThreads);
 }
 
-// Hand-off barriers (all kPipeBlock threads): BAR_AGG + (j & 1) -- the compute
-// warps arrive once tile j's aggregate is in shared memory, the look-back warp
-// waits; BAR_EXCL + (j & 1) -- the look-back warp arrives once tile j's offset
-// is in shared memory, the compute warps wait.  bar.arrive orders the
-// producer's prior shared-memory writes before the consumer's bar.sync returns,
-// and a waiting warp issues nothing (no polling).  Two ids per direction keep
-// at most one pending instance per id: the compute warps can only arrive for
-// tile j+2 after waiting for tile j's offset, which the look-back warp
-// publishes only after its wait for tile j completed.
-constexpr int BAR_AGG = 2, BAR_EXCL = 4;
+// Hand-off barriers (all kPipeBlock threads), two ids per kind indexed by the
+// CTA-local tile number j & 1:
+//   BAR_GRAB: compute warps arrive once tile j's id is in shared memory; the
+//             look-back warp waits, then resolves tile j's exclusive prefix
+//             while the compute warps count and decode it;
+//   BAR_AGG:  compute warps arrive once tile j's aggregate is in shared memory;
+//             the look-back warp waits, publishes tile j's inclusive prefix;
+//   BAR_EXCL: the look-back warp arrives once tile j's offset is in shared
+//             memory; the compute warps wait before copying tile j out (during
+//             tile j+1).
+// bar.arrive orders the producer's prior shared-memory writes before the
+// consumer's bar.sync returns, and a waiting warp issues nothing (no polling).
+// At most one instance per id is pending: every arrival for tile j+2 happens
+// after the compute warps waited for tile j's offset, which the look-back warp
+// only publishes after its waits for tile j completed.
+constexpr int BAR_GRAB = 2, BAR_EXCL = 4, BAR_AGG = 6;
 
 template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
   if (threadIdx.x >= kComputeThreads) {
-    // look-back warp: resolves each tile's offset once the compute warps have
-    // counted it (and published its aggregate), hands the offset back
+    const bool leader = threadIdx.x == kComputeThreads;
     for (unsigned j = 0;; j++) {
-      bar_sync(BAR_AGG + (j & 1), kPipeBlock);
-      const unsigned tile = sm.agg_tile[j & 1];
-      if (tile == kSentinel) break;
-      const unsigned agg = sm.agg[j & 1];
+      bar_sync(BAR_GRAB + (j & 1), kPipeBlock);
+      const unsigned tile = sm.lb_tile[j & 1];
+      if (tile >= a.ntiles) break;
       unsigned long long excl = 0;
       if (tile != 0) {
 #ifdef VT_PROBE
@@ -151,20 +155,27 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #endif
         excl = lookback(a.status, a.epoch, tile, a.ctl, C::kTileElems, a.head);
 #ifdef VT_PROBE
-        if (threadIdx.x == kComputeThreads) {
+        if (leader) {
           atomicAdd(&a.ctl->pad[0], (unsigned long long)(clock64() - t0));
           atomicAdd(&a.ctl->pad[1], 1ull);
         }
 #endif
-        if (threadIdx.x == kComputeThreads && excl != ~0ull)
-          store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + agg));
       }
-      if (threadIdx.x == kComputeThreads) sm.excl[j & 1] = excl;
+      bar_sync(BAR_AGG + (j & 1), kPipeBlock);
+      // (the compute warps already published the aggregate, tile 0 its prefix)
+      if (leader && tile != 0 && excl != ~0ull)
+        store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + sm.agg[j & 1]));
+      if (leader) sm.excl[j & 1] = excl;
       bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
     }
   } else {
     // compute warps
-    if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
+    if (threadIdx.x == 0) {
+      const unsigned t = grab_tile(a, C::kTileElems);
+      sm.tile = t;
+      sm.lb_tile[0] = t;
+    }
+    bar_arrive(BAR_GRAB, kPipeBlock);
     unsigned j = 0, prev_agg = 0;
     while (true) {
       ComputeSync::sync();
@@ -177,7 +188,6 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         // publish the aggregate right away (tile 0: the inclusive prefix), so
         // other CTAs' look-backs never wait on this CTA's look-back warp
         store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
-        sm.agg_tile[j & 1] = tile;
         sm.agg[j & 1] = agg;
       }
       bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
@@ -197,12 +207,15 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         if (kNStage == 1) ComputeSync::sync();
       }
       C::emit(a, tc, sm.out[j % kNStage], off);
-      if (threadIdx.x == 0) sm.tile = grab_tile(a, C::kTileElems);
+      if (threadIdx.x == 0) {
+        const unsigned t = grab_tile(a, C::kTileElems);
+        sm.tile = t;
+        sm.lb_tile[(j + 1) & 1] = t;
+      }
+      bar_arrive(BAR_GRAB + ((j + 1) & 1), kPipeBlock);
       prev_agg = agg;
       j++;
     }
-    if (threadIdx.x == 0) sm.agg_tile[j & 1] = kSentinel;
-    bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
     if (j > 0) {
       bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
       copy_tile_out<C>(a, sm.out[(j - 1) % kNStage], sm.excl[(j - 1) & 1], prev_agg);
