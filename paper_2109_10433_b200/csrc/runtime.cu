@@ -25,6 +25,13 @@
 extern "C" uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut);
 extern "C" uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut);
 
+#ifndef VT_PIPE_BUFS
+#define VT_PIPE_BUFS 3
+#endif
+#ifndef VT_PIPE_CHUNK_MB
+#define VT_PIPE_CHUNK_MB 32
+#endif
+
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
@@ -251,7 +258,7 @@ struct HostCtx {
   uint8_t* d_out = nullptr;
   size_t d_in_cap = 0, d_out_cap = 0;
   // chunked pipeline (large host-pointer calls): kPipeBufs streams and buffers
-  static constexpr int kPipeBufs = 3;
+  static constexpr int kPipeBufs = VT_PIPE_BUFS;
   cudaStream_t ps[kPipeBufs] = {};
   cudaEvent_t pev[kPipeBufs] = {};
   uint8_t* pd_in[kPipeBufs] = {};
@@ -314,9 +321,9 @@ int ensure_pinned(uint8_t*& p, size_t& cap, size_t need) {
   return 0;
 }
 
-// Input elements per pipeline chunk (64 MiB of input).
+// Input elements per pipeline chunk (VT_PIPE_CHUNK_MB MiB of input).
 template <class In>
-constexpr uint64_t pipe_chunk() { return (32ull << 20) / sizeof(In); }
+constexpr uint64_t pipe_chunk() { return ((uint64_t)VT_PIPE_CHUNK_MB << 20) / sizeof(In); }
 
 // Large host-pointer calls: the input is cut at character boundaries into
 // 32 MiB chunks (SURVEY.md 8(a) rules D/E, the same split as the sharder) and

@@ -44,7 +44,11 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+#ifdef VT_EXP_NOSTS
+  asm volatile("" ::"r"(a), "r"(v));
+#else
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
+#endif
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)(v & 0xFF)));

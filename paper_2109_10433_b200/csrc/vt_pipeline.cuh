@@ -119,6 +119,9 @@ template <class C>
 __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const uint8_t* stage,
                                               unsigned long long excl, unsigned agg) {
   if (excl == ~0ull) return;  // a tile before this one failed: output is dead
+#ifdef VT_EXP_NOCOPY
+  return;
+#endif
   copy_out(reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes, stage, agg * C::kOutBytes,
            kComputeThreads);
 }
@@ -206,7 +209,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         copy_tile_out<C>(a, sm.out[(j - 1) % kNStage], sm.excl[(j - 1) & 1], prev_agg);
         if (kNStage == 1) ComputeSync::sync();
       }
+#ifndef VT_EXP_NOEMIT
       C::emit(a, tc, sm.out[j % kNStage], off);
+#endif
       if (threadIdx.x == 0) {
         const unsigned t = grab_tile(a, C::kTileElems);
         sm.tile = t;
