@@ -15,6 +15,9 @@
 //                                                         fields count CPU branches)
 //   utf8_to_utf16.hpp:29-33 utf8_to_utf16 (2 overloads)   GPU, always validating
 //   utf16_to_utf8.hpp:15-17 utf16_to_utf8 (2 overloads)   GPU
+//   validation.hpp:15-24   Utf8BlockValidator            GPU (one launch group per
+//                                                         feed; the chunked form is
+//                                                         vt_utf8_stream_* in vtrans_gpu.h)
 //   validation.hpp:27,31   validate_utf8 / validate_utf16 GPU
 //   vec128.hpp:17-21       Backend, active_backend, ...   report the GPU backend
 //
@@ -23,6 +26,7 @@
 // vtrans::gpu.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <optional>
@@ -73,6 +77,20 @@ std::vector<uint16_t> utf8_to_utf16(std::span<const uint8_t> input, bool validat
 // UTF-16LE -> UTF-8.  `out` must hold 3 * input.size() + 16 bytes.
 TranscodeResult utf16_to_utf8(std::span<const uint16_t> input, uint8_t* out);
 std::vector<uint8_t> utf16_to_utf8(std::span<const uint16_t> input, TranscodeResult& res);
+
+// Streaming UTF-8 validator over 64-byte blocks, same layout and member
+// meaning as the reference's: `error` is all zero while the stream is valid,
+// `prev_incomplete` all zero when no sequence is left dangling at the end
+// (here: its bytes, then their count at [4]), `prev_input` the last 16 bytes.
+struct Utf8BlockValidator {
+  std::array<uint8_t, 16> error{};
+  std::array<uint8_t, 16> prev_input{};
+  std::array<uint8_t, 16> prev_incomplete{};
+
+  void feed(const uint8_t* block64);
+  bool ok_so_far() const;
+  bool finish() const;
+};
 
 bool validate_utf8(std::span<const uint8_t> bytes);
 std::optional<std::size_t> validate_utf16(std::span<const uint16_t> units);

@@ -106,6 +106,40 @@ int vt_host_transcode_bytes(const uint8_t* in, uint64_t n, int from, int to, int
                             uint8_t* out, uint64_t out_cap, uint64_t* out_len, int* exit_code,
                             int* status, int64_t* error_at);
 
+/* ---- streaming UTF-8 validation -------------------------------------------
+ * The GPU form of vtrans::Utf8BlockValidator (proj/include/vtrans/
+ * validation.hpp:15-24, proj/src/validation.cpp:13-22,82-93): chunks of any
+ * length are fed in order; a character may straddle chunk seams.  The state
+ * is 32 bytes, zero-initialised (vt_utf8_stream_init), and lives in device
+ * memory for the _async call or host memory for the vt_host_ call.
+ *   ok so far  <=> error_at < 0
+ *   finish     <=> error_at < 0 && carry_len == 0   (no dangling sequence)
+ * error_at is the first invalid byte in stream coordinates, the same index
+ * whole-buffer validation of the concatenated chunks reports (rule A of
+ * SURVEY.md 8(a)); a sequence cut by the end of the stream so far is not an
+ * error until finish. */
+typedef struct vt_utf8_stream {
+  uint64_t fed;       /* bytes fed so far */
+  int64_t error_at;   /* -1 = valid so far */
+  uint8_t carry[4];   /* the incomplete trailing sequence (carry_len bytes) */
+  uint32_t carry_len;
+  uint32_t skip;      /* scratch for the current feed */
+  uint32_t reserved;
+} vt_utf8_stream;
+
+void vt_utf8_stream_init(vt_utf8_stream* st);
+int vt_utf8_stream_feed_async(vt_utf8_stream* d_st, const uint8_t* d_chunk, uint64_t n,
+                              vt_stream stream);
+int vt_host_utf8_stream_feed(vt_utf8_stream* st, const uint8_t* chunk, uint64_t n);
+int vt_utf8_stream_ok(const vt_utf8_stream* st);      /* host state: 1 = valid so far */
+int vt_utf8_stream_finish(const vt_utf8_stream* st);  /* host state: 1 = valid and complete */
+
+/* ---- corpus statistics -----------------------------------------------------
+ * vtrans::harness::compute_stats (proj/include/vtrans/harness.hpp:47-55,
+ * proj/src/harness.cpp): counts[0..3] = number of 1/2/3/4-byte characters of
+ * a valid buffer; *valid = 0 (and counts zero) when it is not valid UTF-8. */
+int vt_host_utf8_class_counts(const uint8_t* in, uint64_t n, uint64_t counts[4], int* valid);
+
 /* ---- batched short strings ------------------------------------------------
  * `count` strings back to back in `d_data`; string i is
  * [d_offsets[i], d_offsets[i+1]).  Writes the first error index or -1. */

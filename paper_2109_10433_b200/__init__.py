@@ -41,6 +41,12 @@ class _CRes(C.Structure):
     _fields_ = [("consumed", C.c_uint64), ("written", C.c_uint64), ("error_at", C.c_int64)]
 
 
+class _VStream(C.Structure):
+    """vt_utf8_stream (include/vtrans_gpu.h)."""
+    _fields_ = [("fed", C.c_uint64), ("error_at", C.c_int64), ("carry", C.c_uint8 * 4),
+                ("carry_len", C.c_uint32), ("skip", C.c_uint32), ("reserved", C.c_uint32)]
+
+
 @dataclass(frozen=True)
 class TranscodeResult:
     """vtrans::TranscodeResult (proj/include/vtrans/codec_core.hpp:14-21)."""
@@ -107,6 +113,13 @@ def lib():
         "vt_gen_chunk_draws": (C.c_uint64, [C.c_int]),
         "vt_gen_host_chunk": (C.c_uint64, [C.c_int, C.c_uint64, C.c_uint64, _vp, C.c_uint64,
                                            C.POINTER(C.c_uint64)]),
+        "vt_utf8_stream_init": (None, [C.POINTER(_VStream)]),
+        "vt_utf8_stream_feed_async": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
+        "vt_host_utf8_stream_feed": (C.c_int, [C.POINTER(_VStream), _vp, C.c_uint64]),
+        "vt_utf8_stream_ok": (C.c_int, [C.POINTER(_VStream)]),
+        "vt_utf8_stream_finish": (C.c_int, [C.POINTER(_VStream)]),
+        "vt_host_utf8_class_counts": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_uint64 * 4),
+                                                C.POINTER(C.c_int)]),
         "vt_status_string": (C.c_char_p, [C.c_int]),
         "vt_device_count": (C.c_int, []),
         "vt_launch_count": (C.c_uint64, []),
@@ -413,6 +426,66 @@ def generate_host_chunk(cfg: int, seed: int, chunk: int) -> tuple[np.ndarray, Op
     fb = C.c_uint64()
     k = int(L.vt_gen_host_chunk(cfg, seed, chunk, out.ctypes.data, cap, C.byref(fb)))
     return out[:k], (None if fb.value == 0xFFFFFFFFFFFFFFFF else int(fb.value))
+
+
+class Utf8StreamValidator:
+    """Streaming UTF-8 validation on the GPU: the chunked form of
+    vtrans::Utf8BlockValidator (proj/include/vtrans/validation.hpp:15-24).
+
+    Chunks of any length are fed in order (host bytes / numpy arrays, or uint8
+    CUDA tensors, which stay on the device); characters may straddle chunk
+    seams.  ``ok_so_far()`` and ``finish()`` have the reference's meaning;
+    ``error_at`` is the first invalid byte in stream coordinates (what
+    whole-buffer validation of the concatenation reports), or None."""
+
+    def __init__(self):
+        self._st = _VStream()
+        lib().vt_utf8_stream_init(C.byref(self._st))
+        self._dev = None
+
+    def feed(self, chunk, n: Optional[int] = None, stream=None) -> None:
+        if hasattr(chunk, "is_cuda") and chunk.is_cuda:
+            import torch
+
+            n = chunk.numel() if n is None else n
+            if self._dev is None:
+                self._dev = torch.empty(C.sizeof(_VStream), dtype=torch.uint8, device=chunk.device)
+            host = torch.frombuffer(bytearray(bytes(self._st)), dtype=torch.uint8)
+            s = stream if stream is not None else torch.cuda.current_stream()
+            self._dev.copy_(host, non_blocking=False)
+            _check(lib().vt_utf8_stream_feed_async(self._dev.data_ptr(), chunk.data_ptr(), n,
+                                                   int(s.cuda_stream)), "utf8_stream_feed")
+            s.synchronize()
+            C.memmove(C.addressof(self._st), bytes(self._dev.cpu().numpy().tobytes()), C.sizeof(_VStream))
+            return
+        a = _bytes_view(chunk)
+        if n is not None:
+            a = a[:n]
+        _check(lib().vt_host_utf8_stream_feed(C.byref(self._st), _ptr(a), len(a)), "utf8_stream_feed")
+
+    def ok_so_far(self) -> bool:
+        return bool(lib().vt_utf8_stream_ok(C.byref(self._st)))
+
+    def finish(self) -> bool:
+        return bool(lib().vt_utf8_stream_finish(C.byref(self._st)))
+
+    @property
+    def error_at(self) -> Optional[int]:
+        return None if self._st.error_at < 0 else int(self._st.error_at)
+
+    @property
+    def fed(self) -> int:
+        return int(self._st.fed)
+
+
+def utf8_class_counts(data) -> Optional[tuple[int, int, int, int]]:
+    """Numbers of 1/2/3/4-byte characters of valid UTF-8 (GPU), None if invalid."""
+    a = _bytes_view(data)
+    counts = (C.c_uint64 * 4)()
+    valid = C.c_int()
+    _check(lib().vt_host_utf8_class_counts(_ptr(a), len(a), C.byref(counts), C.byref(valid)),
+           "utf8_class_counts")
+    return tuple(int(x) for x in counts) if valid.value else None
 
 
 def launch_count() -> int:

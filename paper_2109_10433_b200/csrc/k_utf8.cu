@@ -44,34 +44,6 @@ __device__ __forceinline__ unsigned leadlen(unsigned b) {
   return b < 0xC0u ? 1u : b < 0xE0u ? 2u : b < 0xF0u ? 3u : b < 0xF8u ? 4u : 1u;
 }
 
-// proj/src/codec_core.cpp:5-38 on a 4-byte window (bytes past the input are
-// zero, which fails exactly like the truncation test at :28).
-__device__ __forceinline__ bool decode_ok(uint32_t v) {
-  const unsigned b0 = v & 0xFF, b1 = (v >> 8) & 0xFF, b2 = (v >> 16) & 0xFF, b3 = v >> 24;
-  if (b0 < 0x80u) return true;
-  unsigned len, cp, lo;
-  if ((b0 & 0xE0u) == 0xC0u) {
-    len = 2; cp = b0 & 0x1Fu; lo = 0x80u;
-  } else if ((b0 & 0xF0u) == 0xE0u) {
-    len = 3; cp = b0 & 0x0Fu; lo = 0x800u;
-  } else if ((b0 & 0xF8u) == 0xF0u) {
-    len = 4; cp = b0 & 0x07u; lo = 0x10000u;
-  } else {
-    return false;
-  }
-  if ((b1 & 0xC0u) != 0x80u) return false;
-  cp = (cp << 6) | (b1 & 0x3Fu);
-  if (len >= 3) {
-    if ((b2 & 0xC0u) != 0x80u) return false;
-    cp = (cp << 6) | (b2 & 0x3Fu);
-  }
-  if (len == 4) {
-    if ((b3 & 0xC0u) != 0x80u) return false;
-    cp = (cp << 6) | (b3 & 0x3Fu);
-  }
-  return cp >= lo && cp <= 0x10FFFFu && (cp < 0xD800u || cp > 0xDFFFu);
-}
-
 // Input description passed by value to out-of-line helpers (a reference to
 // the kernel parameters would force a local-memory copy of them).
 struct Src {
@@ -446,6 +418,17 @@ struct Utf8Codec {
 };
 
 __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Args a) {
+  if (a.skip) {
+    // streaming validator: the first *skip bytes completed the previous
+    // chunk's trailing character (k_stream.cu) and are not part of this scan
+    const unsigned s = *a.skip;
+    if (s == kSkipAll) {
+      a.n = 0;
+    } else {
+      a.head += s;
+      a.n -= s;
+    }
+  }
   validate_body<Utf8Codec<false>>(a);
 }
 

@@ -148,7 +148,8 @@ int grid_for(unsigned tiles, int occ, int sms) {
 
 // Enqueues one UTF-8 kernel; the caller holds sc.mu.
 int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint64_t n,
-                    uint16_t* d_out, vt_result* d_res, cudaStream_t s, int mode) {
+                    uint16_t* d_out, vt_result* d_res, cudaStream_t s, int mode,
+                    const unsigned* d_skip = nullptr) {
   const bool transcode = mode != vt::kModeValidate;
   if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
   vt::U8Args a;
@@ -163,6 +164,7 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
   }();
   a.dbg = dbg;
   a.k = vt::shr_k();
+  a.skip = d_skip;
   VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
   a.out = d_out;
   a.status = sc->status;
@@ -254,6 +256,10 @@ struct HostCtx {
   uint8_t* h_out = nullptr;  // pinned, mapped
   vt_result* h_res = nullptr;
   vt_result* d_res = nullptr;
+  vt_utf8_stream* h_vs = nullptr;  // pinned: streaming-validator state in flight
+  vt_utf8_stream* d_vs = nullptr;
+  unsigned long long* d_counts = nullptr;  // 4 class counters
+  unsigned long long* h_counts = nullptr;
   uint8_t* d_in = nullptr;
   uint8_t* d_out = nullptr;
   size_t d_in_cap = 0, d_out_cap = 0;
@@ -288,6 +294,10 @@ int host_ctx(HostCtx*& out) {
     VT_TRY(cudaHostAlloc(&c.h_out, 3 * kZeroCopyMax + 64, cudaHostAllocMapped));
     VT_TRY(cudaHostAlloc(&c.h_res, sizeof(vt_result), cudaHostAllocMapped));
     VT_TRY(cudaMalloc(&c.d_res, sizeof(vt_result)));
+    VT_TRY(cudaHostAlloc(&c.h_vs, sizeof(vt_utf8_stream), cudaHostAllocDefault));
+    VT_TRY(cudaMalloc(&c.d_vs, sizeof(vt_utf8_stream)));
+    VT_TRY(cudaHostAlloc(&c.h_counts, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
+    VT_TRY(cudaMalloc(&c.d_counts, 4 * sizeof(unsigned long long)));
     c.dev = dev;
   }
   out = &c;
@@ -932,6 +942,98 @@ int vt_debug_probe(vt_stream stream, uint64_t* out5) {
 const char* vt_build_info(void) {
   return "libvtrans_gpu sm_100a (nvcc " VT_STR(__CUDACC_VER_MAJOR__) "." VT_STR(
       __CUDACC_VER_MINOR__) ")";
+}
+
+// ---- streaming UTF-8 validation ----------------------
+
+void vt_utf8_stream_init(vt_utf8_stream* st) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  st->error_at = -1;
+}
+
+int vt_utf8_stream_ok(const vt_utf8_stream* st) { return st && st->error_at < 0 ? 1 : 0; }
+
+int vt_utf8_stream_finish(const vt_utf8_stream* st) {
+  return st && st->error_at < 0 && st->carry_len == 0 ? 1 : 0;
+}
+
+int vt_utf8_stream_feed_async(vt_utf8_stream* d_st, const uint8_t* d_chunk, uint64_t n,
+                              vt_stream stream) {
+  if (!d_st || (n && !d_chunk)) return VT_E_ARG;
+  if (n == 0) return 0;
+  const cudaStream_t s = (cudaStream_t)stream;
+  Target t;
+  VT_TRY(target(s, t));
+  std::lock_guard<std::mutex> lk(t.sc->mu);
+  if (!t.sc->d_res) {
+    VT_TRY(cudaMalloc(&t.sc->d_res, sizeof(vt_result)));
+    VT_TRY(cudaMallocHost(&t.sc->h_res, sizeof(vt_result)));
+  }
+  VT_TRY(vt::launch_stream_seam(d_st, d_chunk, n, s));
+  VT_TRY(run_utf8_locked(t.sc, t.di, d_chunk, n, nullptr, t.sc->d_res, s, vt::kModeValidate,
+                         &d_st->skip));
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  return vt::launch_stream_tail(d_st, d_chunk, n, t.sc->d_res, s);
+}
+
+int vt_host_utf8_stream_feed(vt_utf8_stream* st, const uint8_t* chunk, uint64_t n) {
+  if (!st || (n && !chunk)) return VT_E_ARG;
+  if (n == 0) return 0;
+  HostCtx* c;
+  VT_TRY(host_ctx(c));
+  const uint8_t* d_chunk;
+  if (n <= kZeroCopyMax) {
+    std::memcpy(c->h_in, chunk, n);
+    VT_TRY(cudaHostGetDevicePointer((void**)&d_chunk, c->h_in, 0));
+  } else {
+    VT_TRY(ensure_dev(c->d_in, c->d_in_cap, n, c->stream));
+    VT_TRY(cudaMemcpyAsync(c->d_in, chunk, n, cudaMemcpyHostToDevice, c->stream));
+    d_chunk = c->d_in;
+  }
+  *c->h_vs = *st;
+  VT_TRY(cudaMemcpyAsync(c->d_vs, c->h_vs, sizeof(vt_utf8_stream), cudaMemcpyHostToDevice,
+                         c->stream));
+  VT_TRY(vt_utf8_stream_feed_async(c->d_vs, d_chunk, n, (vt_stream)c->stream));
+  VT_TRY(cudaMemcpyAsync(c->h_vs, c->d_vs, sizeof(vt_utf8_stream), cudaMemcpyDeviceToHost,
+                         c->stream));
+  VT_TRY(cudaStreamSynchronize(c->stream));
+  *st = *c->h_vs;
+  return 0;
+}
+
+// ---- character-class counts (harness::compute_stats) -------------------------
+
+int vt_host_utf8_class_counts(const uint8_t* in, uint64_t n, uint64_t counts[4], int* valid) {
+  if (!counts || !valid || (n && !in)) return VT_E_ARG;
+  for (int i = 0; i < 4; i++) counts[i] = 0;
+  *valid = 1;
+  if (n == 0) return 0;
+  HostCtx* c;
+  VT_TRY(host_ctx(c));
+  const uint8_t* d;
+  if (n <= kZeroCopyMax) {
+    std::memcpy(c->h_in, in, n);
+    VT_TRY(cudaHostGetDevicePointer((void**)&d, c->h_in, 0));
+  } else {
+    VT_TRY(ensure_dev(c->d_in, c->d_in_cap, n, c->stream));
+    VT_TRY(cudaMemcpyAsync(c->d_in, in, n, cudaMemcpyHostToDevice, c->stream));
+    d = c->d_in;
+  }
+  VT_TRY(run_utf8(d, n, nullptr, c->d_res, c->stream, vt::kModeValidate));
+  VT_TRY(cudaMemsetAsync(c->d_counts, 0, 4 * sizeof(unsigned long long), c->stream));
+  VT_TRY(vt::launch_utf8_class_counts(d, n, c->d_counts, c->stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  VT_TRY(cudaMemcpyAsync(c->h_res, c->d_res, sizeof(vt_result), cudaMemcpyDeviceToHost, c->stream));
+  VT_TRY(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, c->stream));
+  VT_TRY(cudaStreamSynchronize(c->stream));
+  if (c->h_res->error_at >= 0) {
+    *valid = 0;
+    return 0;
+  }
+  for (int i = 0; i < 4; i++) counts[i] = c->h_counts[i];
+  return 0;
 }
 
 }  // extern "C"

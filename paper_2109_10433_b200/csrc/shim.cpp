@@ -5,6 +5,7 @@
 // done by the sm_100a kernels behind vt_host_*.  Device/runtime failures, which
 // the reference API cannot express, throw std::runtime_error.
 #include <atomic>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -66,6 +67,34 @@ std::vector<uint8_t> utf16_to_utf8(std::span<const uint16_t> input, TranscodeRes
   res = utf16_to_utf8(input, out.data());
   out.resize(res.written);
   return out;
+}
+
+void Utf8BlockValidator::feed(const uint8_t* block64) {
+  vt_utf8_stream st;
+  vt_utf8_stream_init(&st);
+  if (error[0]) st.error_at = 0;  // (no index at this layer)
+  st.carry_len = prev_incomplete[4];
+  std::memcpy(st.carry, prev_incomplete.data(), 4);
+  check(vt_host_utf8_stream_feed(&st, block64, 64), "Utf8BlockValidator::feed");
+  error.fill(0);
+  error[0] = st.error_at >= 0 ? 1 : 0;
+  prev_incomplete.fill(0);
+  std::memcpy(prev_incomplete.data(), st.carry, st.carry_len);
+  prev_incomplete[4] = (uint8_t)st.carry_len;
+  std::memcpy(prev_input.data(), block64 + 48, 16);
+}
+
+bool Utf8BlockValidator::ok_so_far() const {
+  for (uint8_t b : error)
+    if (b) return false;
+  return true;
+}
+
+bool Utf8BlockValidator::finish() const {
+  if (!ok_so_far()) return false;
+  for (uint8_t b : prev_incomplete)
+    if (b) return false;
+  return true;
 }
 
 bool validate_utf8(std::span<const uint8_t> bytes) {

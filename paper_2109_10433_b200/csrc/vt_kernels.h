@@ -36,6 +36,7 @@ struct U8Args {
   vt_result* res;
   unsigned dbg;  // debug switches (VT_DEBUG env), 0 in production
   ShrK k;
+  const unsigned* skip;  // validate only: device count of leading bytes to skip, or null
 };
 
 // UTF-16 side: same conventions in units (`head` in units, 0..7).
@@ -66,6 +67,17 @@ unsigned tiles_utf16(unsigned long long head, unsigned long long n);
 // Batched validation of many short strings (one warp per string).
 int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
                                int64_t* first_err, cudaStream_t s);
+// skip value meaning "nothing of this chunk is scanned" (the stream failed)
+constexpr unsigned kSkipAll = 0xFFFFFFFFu;
+// Streaming UTF-8 validation (k_stream.cu): seam check before, carry/error
+// update after a validate launch over the chunk (with a.skip = &st->skip).
+int launch_stream_seam(vt_utf8_stream* st, const uint8_t* chunk, uint64_t n, cudaStream_t s);
+int launch_stream_tail(vt_utf8_stream* st, const uint8_t* chunk, uint64_t n, const vt_result* res,
+                       cudaStream_t s);
+// Character-length histogram of valid UTF-8 (k_stream.cu): counts[0..3] +=
+// number of 1/2/3/4-byte characters.
+int launch_utf8_class_counts(const uint8_t* d, uint64_t n, unsigned long long* counts,
+                             cudaStream_t s);
 // Byte swap of n UTF-16 units (device buffers, 4-byte aligned).
 int launch_bswap16(const uint16_t* in, uint16_t* out, uint64_t n, cudaStream_t s);
 // Every 1/2/3-byte input (acceptance C3 order), verdict per input.

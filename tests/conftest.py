@@ -32,3 +32,11 @@ def golden():
     with open(os.path.join(d, "misc.json")) as f:
         misc = json.load(f)
     return {"u8": u8, "u16": u16, "misc": misc}
+
+
+@pytest.fixture(scope="session")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch

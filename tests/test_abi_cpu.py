@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     import ctypes
 
     hdr = open(os.path.join(ROOT, "include", "vtrans_gpu.h")).read()
-    names = sorted(set(re.findall(r"^\s*(?:int|uint64_t|const char\*)\s+(vt_\w+)\(", hdr, re.M)))
+    names = sorted(set(re.findall(r"^\s*(?:int|void|uint64_t|const char\*)\s+(vt_\w+)\(", hdr, re.M)))
     assert len(names) >= 28, names
     L = ctypes.CDLL(vt.LIB_PATH)
     missing = [n for n in names if not hasattr(L, n)]
@@ -47,6 +47,9 @@ def test_drop_in_cxx_symbols_exported():
         "_ZN6vtrans14active_backendEv",
         "_ZN6vtrans24native_backend_availableEv",
         "_ZN6vtrans22force_emulated_backendEb",
+        "_ZN6vtrans18Utf8BlockValidator4feedEPKh",
+        "_ZNK6vtrans18Utf8BlockValidator9ok_so_farEv",
+        "_ZNK6vtrans18Utf8BlockValidator6finishEv",
     ]:
         assert mangled in out, mangled
 
@@ -59,6 +62,10 @@ def test_no_cpu_fallback_without_gpu():
         vt.utf16_to_utf8([0x41])
     with pytest.raises(vt.VtransError):
         vt.validate_utf8(b"")
+    with pytest.raises(vt.VtransError):
+        vt.Utf8StreamValidator().feed(b"\xe2\x82")
+    with pytest.raises(vt.VtransError):
+        vt.utf8_class_counts(b"abc")
     assert vt.device_count() == 0
 
 

@@ -20,14 +20,6 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.fixture(scope="module")
-def torch():
-    import torch
-
-    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    return torch
-
-
 def _u16(hexstr):
     return np.frombuffer(bytes.fromhex(hexstr), dtype="<u2").astype(np.uint16)
 
