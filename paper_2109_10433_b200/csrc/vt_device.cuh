@@ -98,58 +98,111 @@ __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p
 // Warp-cooperative decoupled look-back for tile `tile` (> 0), executed by one
 // full warp.  Returns the exclusive prefix, or ~0ull when the tile became
 // irrelevant (a tile before it reported an error, so its output is never read).
-// Lane i inspects tile base - i (newest first).  When a step finds an inclusive
-// prefix, the warp also publishes the inclusive prefixes of the aggregate-only
-// tiles it summed on the way ("helping"), so the prefix frontier keeps up with
-// the tiles in flight and later look-backs stay one step deep.
+//
+// Each step loads VT_LB_WIN windows of 32 status words at once (window k, lane
+// i: tile base - 32k - i; independent loads, one L2 round trip), then walks
+// them newest first: a fully-ready window without an inclusive prefix is summed
+// and passed, the first window with a prefix ends the walk.  A window that is
+// not ready yet stops the step; the ready part before it is banked and the step
+// repeats from there.  When the prefix is found the warp also publishes the
+// inclusive prefixes of every aggregate-only tile it summed in this step
+// ("helping"), so the prefix frontier keeps up with the tiles in flight.
+//
+// Aggregates are tile-sized (< 2^16 elements, <= 3 output bytes each), so sums
+// over one step's <= 32 * VT_LB_WIN tiles fit in 32 bits (32-bit shuffles, REDUX).
+#ifndef VT_LB_WIN
+#define VT_LB_WIN 1  // measured: 2 and 4 windows per step are slower (L2 contention)
+#endif
+#ifndef VT_LB_SLEEP
+#define VT_LB_SLEEP 2000  // ns between polls of a window that is not ready
+#endif
 __device__ __forceinline__ unsigned long long lookback(unsigned long long* status, unsigned epoch,
                                                       unsigned tile, const Ctl* ctl,
                                                       unsigned long long tile_bytes,
                                                       unsigned long long head) {
+  constexpr int K = VT_LB_WIN;
   const unsigned lane = threadIdx.x & 31;
   const unsigned ep = epoch & 0x3FFF;
   unsigned long long excl = 0;
   long long base = (long long)tile - 1;  // newest predecessor not yet summed
-  unsigned spins = 0;
   while (true) {
-    const long long idx = base - (long long)lane;
-    const unsigned long long s = idx >= 0 ? load_status(&status[idx]) : 0ull;
-    const bool ready = idx < 0 || (((s >> 62) != 0) && (((s >> 48) & 0x3FFF) == ep));
-    const bool is_pre = idx < 0 || (ready && (s >> 62) == 2);  // before tile 0: prefix 0
-    const unsigned long long v = idx < 0 ? 0ull : (s & kValMask);
-    const unsigned rm = __ballot_sync(0xffffffffu, ready);
-    const unsigned pm = __ballot_sync(0xffffffffu, is_pre);
-    const unsigned run = rm == 0xffffffffu ? 32u : (unsigned)__ffs(~rm) - 1u;
-    const unsigned pre_in = pm & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
-    if (pre_in) {
-      const unsigned stop = (unsigned)__ffs(pre_in) - 1u;  // nearest inclusive prefix
-      // suffix sums over lanes [lane, stop): inclusive prefix of tile base - lane
-      unsigned long long x = lane < stop ? v : 0ull;
+    unsigned long long v[K];
+    bool rdy[K], pre[K];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_down_sync(0xffffffffu, x, o);
-        if (lane + o < 32) x += y;
+    for (int k = 0; k < K; k++) {
+      const long long idx = base - 32 * k - (long long)lane;
+      const unsigned long long st = idx >= 0 ? load_status(&status[idx]) : 0ull;
+      rdy[k] = idx < 0 || (((st >> 62) != 0) && (((st >> 48) & 0x3FFF) == ep));
+      pre[k] = idx < 0 || (rdy[k] && (st >> 62) == 2);  // before tile 0: prefix 0
+      v[k] = idx < 0 ? 0ull : (st & kValMask);
+    }
+    uint32_t wsum[K];  // window sums of the fully-ready windows passed so far
+    int k = 0;
+    unsigned run = 0;
+#pragma unroll
+    for (int kk = 0; kk < K; kk++) {
+      k = kk;
+      const unsigned rm = __ballot_sync(0xffffffffu, rdy[kk]);
+      const unsigned pm = __ballot_sync(0xffffffffu, pre[kk]);
+      run = rm == 0xffffffffu ? 32u : (unsigned)__ffs(~rm) - 1u;
+      const unsigned pre_in = pm & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
+      if (pre_in) {
+        const unsigned stop = (unsigned)__ffs(pre_in) - 1u;  // nearest inclusive prefix
+        const unsigned long long pval = __shfl_sync(0xffffffffu, v[kk], stop);
+        // window k: suffix sums over lanes [lane, stop)
+        uint32_t x = lane < stop ? (uint32_t)v[kk] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
+          if (lane + o < 32) x += y;
+        }
+        if (lane < stop)
+          store_status(&status[base - 32 * kk - lane], pack_status(kFlagPre, epoch, pval + x));
+        unsigned long long newer = pval + __shfl_sync(0xffffffffu, x, 0);  // prefix through window k
+        // windows k-1 .. 0 (fully ready, summed): their tiles' inclusive prefixes
+#pragma unroll
+        for (int j = kk - 1; j >= 0; j--) {
+          uint32_t z = (uint32_t)v[j];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_down_sync(0xffffffffu, z, o);
+            if (lane + o < 32) z += y;
+          }
+          store_status(&status[base - 32 * j - lane], pack_status(kFlagPre, epoch, newer + z));
+          newer += wsum[j];
+        }
+        return excl + newer;
       }
-      const unsigned long long pval = __shfl_sync(0xffffffffu, v, stop);
-      if (lane < stop) store_status(&status[idx], pack_status(kFlagPre, epoch, pval + x));
-      // this tile's exclusive prefix: everything newer than the prefix tile
-      return excl + __shfl_sync(0xffffffffu, x, 0) + pval;
+      if (run < 32) break;
+      wsum[kk] = __reduce_add_sync(0xffffffffu, (uint32_t)v[kk]);
+      k = kk + 1;
     }
 #ifdef VT_PROBE
-    if (lane == 0) atomicAdd(const_cast<unsigned long long*>(&ctl->pad[4]), run > 0 ? (1ull << 32) : 1ull);
+    if (lane == 0) atomicAdd(const_cast<unsigned long long*>(&ctl->pad[4]), (k > 0 || run > 0) ? (1ull << 32) : 1ull);
 #endif
-    if (run > 0) {
-      unsigned long long t = lane < run ? v : 0ull;
+    // no prefix in reach: bank the ready part (windows 0..k-1, then `run` lanes of k)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      excl += t;
-      base -= (long long)run;
+    for (int j = 0; j < K; j++)
+      if (j < k) excl += wsum[j];
+    unsigned long long adv = 32ull * k;
+    if (k < K && run > 0) {
+      uint32_t part = 0;
+#pragma unroll
+      for (int j = 0; j < K; j++)
+        if (j == k) part = __reduce_add_sync(0xffffffffu, lane < run ? (uint32_t)v[j] : 0u);
+      excl += part;
+      adv += run;
+    }
+    if (adv > 0) {
+      base -= (long long)adv;
       continue;
     }
     // nothing ready yet: give up if an earlier tile failed (our output is dead)
     const unsigned long long e = load_relaxed(const_cast<unsigned long long*>(&ctl->err));
     if (e != kNoError && (e + head) / tile_bytes < tile) return ~0ull;
-    if (++spins > 8) __nanosleep(32);
+    // back off: the status lines are hot in L2 (hundreds of look-backs poll
+    // them); measured best with a long sleep, the slack is more than a tile
+    __nanosleep(VT_LB_SLEEP);
   }
 }
 
