@@ -106,6 +106,21 @@ int vt_host_transcode_bytes(const uint8_t* in, uint64_t n, int from, int to, int
                             uint8_t* out, uint64_t out_cap, uint64_t* out_len, int* exit_code,
                             int* status, int64_t* error_at);
 
+/* ---- output lengths ---------------------------------------------------------
+ * How many elements the transcoding would write: UTF-16 units of a UTF-8 input
+ * (characters + supplementary characters), UTF-8 bytes of a UTF-16 input.
+ * As for validation, res.written holds the length of the valid prefix and
+ * res.error_at the first invalid index (-1 if none); the host forms return -1
+ * for invalid input.  One read of the input, no output written. */
+int vt_utf16_len_from_utf8_async(const uint8_t* d_in, uint64_t n, vt_result* d_res,
+                                 vt_stream stream);
+int vt_utf8_len_from_utf16_async(const uint16_t* d_in, uint64_t n, vt_result* d_res,
+                                 vt_stream stream);
+int vt_utf16_len_from_utf8(const uint8_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream);
+int vt_utf8_len_from_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream);
+int vt_host_utf16_len_from_utf8(const uint8_t* in, uint64_t n, int64_t* len);
+int vt_host_utf8_len_from_utf16(const uint16_t* in, uint64_t n, int64_t* len);
+
 /* ---- streaming UTF-8 validation -------------------------------------------
  * The GPU form of vtrans::Utf8BlockValidator (proj/include/vtrans/
  * validation.hpp:15-24, proj/src/validation.cpp:13-22,82-93): chunks of any

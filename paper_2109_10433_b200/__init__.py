@@ -113,6 +113,12 @@ def lib():
         "vt_gen_chunk_draws": (C.c_uint64, [C.c_int]),
         "vt_gen_host_chunk": (C.c_uint64, [C.c_int, C.c_uint64, C.c_uint64, _vp, C.c_uint64,
                                            C.POINTER(C.c_uint64)]),
+        "vt_utf16_len_from_utf8_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+        "vt_utf8_len_from_utf16_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp]),
+        "vt_utf16_len_from_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(_CRes), _vp]),
+        "vt_utf8_len_from_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(_CRes), _vp]),
+        "vt_host_utf16_len_from_utf8": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
+        "vt_host_utf8_len_from_utf16": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int64)]),
         "vt_utf8_stream_init": (None, [C.POINTER(_VStream)]),
         "vt_utf8_stream_feed_async": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
         "vt_host_utf8_stream_feed": (C.c_int, [C.POINTER(_VStream), _vp, C.c_uint64]),
@@ -216,6 +222,22 @@ def count_utf16(units) -> Optional[int]:
 
 
 # ---- UTF-16 big-endian and byte-order marks --------------------------------------
+
+def utf16_len_from_utf8(data) -> Optional[int]:
+    """UTF-16 units the transcoding of valid UTF-8 writes, None if invalid (GPU)."""
+    a = _bytes_view(data)
+    n = C.c_int64()
+    _check(lib().vt_host_utf16_len_from_utf8(_ptr(a), len(a), C.byref(n)), "utf16_len_from_utf8")
+    return None if n.value < 0 else int(n.value)
+
+
+def utf8_len_from_utf16(units) -> Optional[int]:
+    """UTF-8 bytes the transcoding of valid UTF-16 writes, None if invalid (GPU)."""
+    a = _units_view(units)
+    n = C.c_int64()
+    _check(lib().vt_host_utf8_len_from_utf16(_ptr(a), len(a), C.byref(n)), "utf8_len_from_utf16")
+    return None if n.value < 0 else int(n.value)
+
 
 def utf8_to_utf16be(data):
     """UTF-8 -> UTF-16BE units (as host-order uint16 values holding the
@@ -323,6 +345,22 @@ def validate_utf16_device(d_in, n: int, stream=None, d_res=None, offset: int = 0
         return None
     r = _CRes()
     _check(lib().vt_validate_utf16(p, n, C.byref(r), _stream_ptr(stream)), "validate_utf16")
+    return TranscodeResult._of(r)
+
+
+def utf16_len_from_utf8_device(d_in, n: int, stream=None, offset: int = 0) -> "TranscodeResult":
+    """Length of the UTF-16 transcoding of ``n`` bytes on the device: ``written``
+    of the valid prefix, ``error_at`` as for validation."""
+    r = _CRes()
+    _check(lib().vt_utf16_len_from_utf8(d_in.data_ptr() + offset, n, C.byref(r), _stream_ptr(stream)),
+           "utf16_len_from_utf8")
+    return TranscodeResult._of(r)
+
+
+def utf8_len_from_utf16_device(d_in, n: int, stream=None, offset: int = 0) -> "TranscodeResult":
+    r = _CRes()
+    _check(lib().vt_utf8_len_from_utf16(d_in.data_ptr() + offset, n, C.byref(r), _stream_ptr(stream)),
+           "utf8_len_from_utf16")
     return TranscodeResult._of(r)
 
 

@@ -319,9 +319,9 @@ struct Utf16Codec {
   }
 };
 
-template <bool kBE>
+template <bool kBE, bool kUnits = false>
 __global__ void __launch_bounds__(kComputeThreads, 4) utf16_validate_kernel(U16Args a) {
-  validate_body<Utf16Codec<kBE>>(a);
+  validate_body<Utf16Codec<kBE>, kUnits>(a);
 }
 
 // UTF-16LE (kBE = false) or UTF-16BE (kBE = true) -> UTF-8
@@ -353,6 +353,8 @@ int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s) {
     utf16_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec<true>>), s>>>(a);
   else if (mode == kModeValidateBE)
     utf16_validate_kernel<true><<<grid, kComputeThreads, 0, s>>>(a);
+  else if (mode == kModeLength)
+    utf16_validate_kernel<false, true><<<grid, kComputeThreads, 0, s>>>(a);
   else
     utf16_validate_kernel<false><<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();

@@ -417,6 +417,7 @@ struct Utf8Codec {
   }
 };
 
+template <bool kUnits>
 __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Args a) {
   if (a.skip) {
     // streaming validator: the first *skip bytes completed the previous
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Arg
       a.n -= s;
     }
   }
-  validate_body<Utf8Codec<false>>(a);
+  validate_body<Utf8Codec<false>, kUnits>(a);
 }
 
 #ifndef VT_K8_MINB
@@ -459,8 +460,10 @@ int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s) {
     utf8_transcode_kernel<false><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<false>>), s>>>(a);
   else if (mode == kModeTranscodeBE)
     utf8_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<true>>), s>>>(a);
+  else if (mode == kModeLength)
+    utf8_validate_kernel<true><<<grid, kComputeThreads, 0, s>>>(a);
   else
-    utf8_validate_kernel<<<grid, kComputeThreads, 0, s>>>(a);
+    utf8_validate_kernel<false><<<grid, kComputeThreads, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -471,7 +474,7 @@ int occupancy_utf8(bool transcode) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel<false>, kPipeBlock,
                                                   sizeof(PipeSmem<Utf8Codec<false>>));
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel, kComputeThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel<false>, kComputeThreads, 0);
   }
   return n;
 }

@@ -150,7 +150,7 @@ int grid_for(unsigned tiles, int occ, int sms) {
 int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint64_t n,
                     uint16_t* d_out, vt_result* d_res, cudaStream_t s, int mode,
                     const unsigned* d_skip = nullptr) {
-  const bool transcode = mode != vt::kModeValidate;
+  const bool transcode = mode == vt::kModeTranscode || mode == vt::kModeTranscodeBE;
   if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
   vt::U8Args a;
   const uintptr_t p = (uintptr_t)d_in;
@@ -559,6 +559,52 @@ int vt_validate_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_str
   return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
     return run_utf16_locked(sc, di, d_in, n, nullptr, d, s, vt::kModeValidate);
   });
+}
+
+// ---- output lengths (vt_utf16_len_from_utf8 / vt_utf8_len_from_utf16)
+
+int vt_utf16_len_from_utf8_async(const uint8_t* d_in, uint64_t n, vt_result* d_res,
+                                 vt_stream stream) {
+  return run_utf8(d_in, n, nullptr, d_res, (cudaStream_t)stream, vt::kModeLength);
+}
+
+int vt_utf8_len_from_utf16_async(const uint16_t* d_in, uint64_t n, vt_result* d_res,
+                                 vt_stream stream) {
+  return run_utf16(d_in, n, nullptr, d_res, (cudaStream_t)stream, vt::kModeLength);
+}
+
+int vt_utf16_len_from_utf8(const uint8_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf8_locked(sc, di, d_in, n, nullptr, d, s, vt::kModeLength);
+  });
+}
+
+int vt_utf8_len_from_utf16(const uint16_t* d_in, uint64_t n, vt_result* h_res, vt_stream stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  return sync_result(s, h_res, [&](Scratch* sc, const DeviceInfo& di, vt_result* d) {
+    return run_utf16_locked(sc, di, d_in, n, nullptr, d, s, vt::kModeLength);
+  });
+}
+
+int vt_host_utf16_len_from_utf8(const uint8_t* in, uint64_t n, int64_t* len) {
+  if (!len) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint8_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf8(i, k, nullptr, d, s, vt::kModeLength);
+  }));
+  *len = r.error_at < 0 ? (int64_t)r.written : -1;
+  return 0;
+}
+
+int vt_host_utf8_len_from_utf16(const uint16_t* in, uint64_t n, int64_t* len) {
+  if (!len) return VT_E_ARG;
+  vt_result r;
+  VT_TRY(host_validate(in, n, &r, [](const uint16_t* i, uint64_t k, vt_result* d, cudaStream_t s) {
+    return run_utf16(i, k, nullptr, d, s, vt::kModeLength);
+  }));
+  *len = r.error_at < 0 ? (int64_t)r.written : -1;
+  return 0;
 }
 
 int vt_host_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, vt_result* res) {

@@ -55,6 +55,9 @@ struct U16Args {
 // launch modes: validate/count, transcode to UTF-16LE / UTF-8, transcode to
 // UTF-16BE (UTF-8 side) / from UTF-16BE (UTF-16 side)
 constexpr int kModeValidate = 0, kModeTranscode = 1, kModeTranscodeBE = 2, kModeValidateBE = 3;
+// length only: the validate kernel counting output elements (UTF-16 units of a
+// UTF-8 input, UTF-8 bytes of a UTF-16 input) instead of code points
+constexpr int kModeLength = 4;
 
 int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf8(bool transcode);

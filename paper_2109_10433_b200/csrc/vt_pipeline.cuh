@@ -75,7 +75,8 @@ __device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems
   return t;
 }
 
-template <class C>
+// kUnits: count output elements (the transcode's `written`) instead of code points.
+template <class C, bool kUnits = false>
 __device__ __forceinline__ void validate_body(const typename C::Args& a) {
   __shared__ unsigned red[kComputeThreads / 32], scan[kComputeThreads / 32];
   __shared__ unsigned tile_s;
@@ -86,7 +87,7 @@ __device__ __forceinline__ void validate_body(const typename C::Args& a) {
     if (tile >= a.ntiles) break;
     typename C::TileCount tc;
     unsigned off, total;
-    C::template count<false, kComputeThreads, SyncAll>(a, tile, red, scan, tc, off, total);
+    C::template count<kUnits, kComputeThreads, SyncAll>(a, tile, red, scan, tc, off, total);
     if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
   }
   finalize_if_last(a, false, C::kTileElems);

@@ -216,3 +216,35 @@ def test_prefix_sweep_cuts_on_character_boundaries():
     assert recs and recs[0].bytes_in == 15 and recs[0].chars == 5
     assert recs[-1].bytes_in == 120 and recs[-1].chars == 40
     assert all(r.reps > 0 for r in recs)
+
+
+def test_output_lengths(oracle, torch):
+    """vt_utf16_len_from_utf8 / vt_utf8_len_from_utf16: the
+    transcoding's `written` without writing output, valid and invalid inputs,
+    all alignments."""
+    rng = random.Random(3)
+    base8, _ = vt.generate_host_chunk(4, 4, 1)
+    base8 = bytes(base8[:200_000])
+    base16, _ = vt.generate_host_chunk(3, 3, 1)
+    base16 = np.asarray(base16[:100_000], dtype=np.uint16)
+    for it in range(40):
+        d = bytearray(base8[: rng.randrange(0, len(base8))])
+        if it % 2 and d:
+            d[rng.randrange(len(d))] = rng.choice([0x80, 0xC0, 0xED, 0xFF, 0xF4])
+        d = bytes(d)
+        _, want = oracle.utf8_to_utf16(d)
+        assert vt.utf16_len_from_utf8(d) == (want.written if want.error_at is None else None)
+        off = it % 16
+        t = torch.zeros(len(d) + 32, dtype=torch.uint8, device="cuda")
+        if d:
+            t[off:off + len(d)] = torch.frombuffer(bytearray(d), dtype=torch.uint8).cuda()
+        r = vt.utf16_len_from_utf8_device(t, len(d), offset=off)
+        assert (r.written, r.error_at) == (want.written, want.error_at), it
+        u = base16[: rng.randrange(0, len(base16))].copy()
+        if it % 2 and len(u):
+            u[rng.randrange(len(u))] = rng.choice([0xD800, 0xDC00, 0xDBFF])
+        _, w16 = oracle.utf16_to_utf8(u)
+        assert vt.utf8_len_from_utf16(u) == (w16.written if w16.error_at is None else None)
+        t16 = torch.from_numpy(np.concatenate([np.zeros(8, np.uint16), u]).view(np.int16)).cuda()
+        r16 = vt.utf8_len_from_utf16_device(t16, len(u), offset=16)
+        assert (r16.written, r16.error_at) == (w16.written, w16.error_at), it
