@@ -120,14 +120,17 @@ int prepare(Scratch& sc, cudaStream_t s, unsigned tiles, unsigned& epoch) {
     VT_TRY(cudaMalloc(&sc.ctl, sizeof(vt::Ctl)));
     vt::Ctl init{};
     init.err = vt::kNoError;
-    VT_TRY(cudaMemcpy(sc.ctl, &init, sizeof init, cudaMemcpyHostToDevice));
+    // stream-ordered: a non-blocking stream does not wait for the legacy
+    // default stream, where the synchronous forms would be queued
+    VT_TRY(cudaMemcpyAsync(sc.ctl, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    VT_TRY(cudaStreamSynchronize(s));  // `init` is a host stack object
   }
   if (tiles > sc.status_cap) {
     VT_TRY(cudaStreamSynchronize(s));  // the old array may still be in use
     if (sc.status) VT_TRY(cudaFree(sc.status));
     size_t cap = std::max<size_t>(tiles, 1u << 16);
     VT_TRY(cudaMalloc(&sc.status, cap * sizeof(unsigned long long)));
-    VT_TRY(cudaMemset(sc.status, 0, cap * sizeof(unsigned long long)));
+    VT_TRY(cudaMemsetAsync(sc.status, 0, cap * sizeof(unsigned long long), s));
     sc.status_cap = cap;
     sc.epoch = 0;
   }
