@@ -417,8 +417,21 @@ struct Utf8Codec {
   }
 };
 
+
+// ---- validation / lengths without barriers ----------------------------------------
+// Validation needs no offsets, so no block scan: each warp takes 2 KiB rows
+// (64 bytes per lane, the same loads and classify as the transcode) in grid
+// stride, keeps its count in registers and records the row's count (one REDUX)
+// for the rare error case.  The only atomics are per error and per CTA.  The
+// last CTA finalises: without an error the total is the answer; with one, the
+// rows before the error row (all valid) are summed from row_counts and the error
+// row is recounted up to the error.  kUnits counts UTF-16 units instead of code
+// points (the length entry points).
+constexpr int K8_ROW = 32 * K8_BPT;  // bytes per warp row
+
 template <bool kUnits>
-__global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Args a) {
+__global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
+  unsigned* const row_counts = a.rows;
   if (a.skip) {
     // streaming validator: the first *skip bytes completed the previous
     // chunk's trailing character (k_stream.cu) and are not part of this scan
@@ -430,7 +443,111 @@ __global__ void __launch_bounds__(kComputeThreads, 4) utf8_validate_kernel(U8Arg
       a.n -= s;
     }
   }
-  validate_body<Utf8Codec<false>, kUnits>(a);
+  __shared__ unsigned long long warp_tot[8];
+  __shared__ bool last;
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  const long long head = (long long)a.head, end = (long long)(a.head + a.n);
+  const unsigned long long nrows = (unsigned long long)(end + K8_ROW - 1) / K8_ROW;
+  const Src src{a.base, a.head, a.n};
+  unsigned long long total = 0;
+  unsigned it = 0;
+  for (unsigned long long row = gw; row < nrows; row += nwarps, it++) {
+    const long long r0 = (long long)row * K8_ROW;
+    if ((it & 3) == 0) {  // stop behind a known error (warp-uniform decision)
+      unsigned long long e = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
+      e = __shfl_sync(0xffffffffu, e, 0);
+      if (e != kNoError && (long long)e + head < r0) break;
+    }
+    const long long v0 = r0 + (long long)K8_BPT * lane;
+    const bool interior = r0 - 4 >= head && r0 + K8_ROW + 4 <= end;
+    Words W;
+    if (interior) {
+      const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
+#pragma unroll
+      for (int r = 0; r < K8_WPT / 4; r++) {
+        const uint4 v = __ldg(p + r);
+        W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y;
+        W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
+      }
+      uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K8_WPT], 1);
+      uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
+      if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 4));
+      if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K8_BPT));
+      W.w[0] = pw;
+      W.w[K8_WPT + 1] = nw;
+    } else {
+      load_masked(src, v0, W);
+    }
+    const ClassOut co = classify(W, a.k);
+    unsigned cnt;
+    if (interior && !co.viol) {
+      cnt = kUnits ? co.units : co.chars;
+    } else {
+      const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
+      const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
+      const unsigned er = first_error_rule_a(src, v0, lo, hi);
+      if (er != kNone) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
+      cnt = generic_chars(src, v0, lo, hi, kUnits, nullptr);
+    }
+    total += cnt;
+    const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) row_counts[row] = rc;
+  }
+  // per-CTA total, one atomic
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0) warp_tot[wib] = total;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; w++) t += warp_tot[w];
+    if (t) atomicAdd(&a.ctl->count, t);
+    __threadfence();
+    last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const unsigned long long e = load_relaxed(&a.ctl->err);
+  unsigned long long written = load_relaxed(&a.ctl->count);
+  if (e != kNoError) {
+    // valid prefix: rows before the error row, then the error row up to e
+    const unsigned long long erow = (e + a.head) / K8_ROW;
+    unsigned long long t = 0;
+    for (unsigned long long r = threadIdx.x; r < erow; r += blockDim.x)
+      t += ((volatile unsigned*)row_counts)[r];
+    if (wib == 0) {
+      const long long v0 = (long long)erow * K8_ROW + (long long)K8_BPT * lane;
+      const long long stop = (long long)e + head;
+      const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
+      const unsigned lim = (unsigned)max((long long)lo, min((long long)K8_BPT, stop - v0));
+      t += generic_chars(src, v0, lo, lim, kUnits, nullptr);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) warp_tot[wib] = t;
+    __syncthreads();
+    written = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; w++) written += warp_tot[w];
+  }
+  if (threadIdx.x == 0) {
+    vt_result r;
+    r.written = written;
+    r.consumed = e == kNoError ? a.n : e;
+    r.error_at = e == kNoError ? -1 : (long long)e;
+    *a.res = r;
+    a.ctl->tile_counter = 0;
+    a.ctl->count = 0;
+    a.ctl->err = kNoError;
+    __threadfence();
+    a.ctl->done = 0;
+  }
+}
+
+unsigned rows_utf8(unsigned long long head, unsigned long long n) {
+  return (unsigned)((head + n + K8_ROW - 1) / K8_ROW);
 }
 
 #ifndef VT_K8_MINB
@@ -461,9 +578,9 @@ int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s) {
   else if (mode == kModeTranscodeBE)
     utf8_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<true>>), s>>>(a);
   else if (mode == kModeLength)
-    utf8_validate_kernel<true><<<grid, kComputeThreads, 0, s>>>(a);
+    utf8_validate_rows_kernel<true><<<grid, 256, 0, s>>>(a);
   else
-    utf8_validate_kernel<false><<<grid, kComputeThreads, 0, s>>>(a);
+    utf8_validate_rows_kernel<false><<<grid, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -474,7 +591,7 @@ int occupancy_utf8(bool transcode) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_transcode_kernel<false>, kPipeBlock,
                                                   sizeof(PipeSmem<Utf8Codec<false>>));
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_kernel<false>, kComputeThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf8_validate_rows_kernel<false>, 256, 0);
   }
   return n;
 }

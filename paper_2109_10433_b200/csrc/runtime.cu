@@ -99,7 +99,19 @@ struct Scratch {
   unsigned epoch = 0;
   vt_result* d_res = nullptr;  // device result slot for the synchronous API
   vt_result* h_res = nullptr;  // pinned host mirror
+  unsigned* rows = nullptr;    // per-row counts of the validate kernels
+  size_t rows_cap = 0;
 };
+
+int ensure_rows(Scratch& sc, cudaStream_t s, size_t rows) {
+  if (rows <= sc.rows_cap) return 0;
+  VT_TRY(cudaStreamSynchronize(s));  // the old array may still be in use
+  if (sc.rows) VT_TRY(cudaFree(sc.rows));
+  const size_t cap = std::max<size_t>(rows, 1u << 19);
+  VT_TRY(cudaMalloc(&sc.rows, cap * sizeof(unsigned)));
+  sc.rows_cap = cap;
+  return 0;
+}
 
 std::mutex g_scratch_mu;
 std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Scratch>> g_scratch;
@@ -168,6 +180,12 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
   a.dbg = dbg;
   a.k = vt::shr_k();
   a.skip = d_skip;
+  a.rows = nullptr;
+  if (!transcode) {
+    const unsigned rows = vt::rows_utf8(a.head, n);
+    VT_TRY(ensure_rows(*sc, s, rows));
+    a.rows = sc->rows;
+  }
   VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
   a.out = d_out;
   a.status = sc->status;

@@ -37,6 +37,7 @@ struct U8Args {
   unsigned dbg;  // debug switches (VT_DEBUG env), 0 in production
   ShrK k;
   const unsigned* skip;  // validate only: device count of leading bytes to skip, or null
+  unsigned* rows;        // validate only: per-row counts scratch (rows_utf8 entries)
 };
 
 // UTF-16 side: same conventions in units (`head` in units, 0..7).
@@ -62,6 +63,7 @@ constexpr int kModeLength = 4;
 int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf8(bool transcode);
 unsigned tiles_utf8(unsigned long long head, unsigned long long n);
+unsigned rows_utf8(unsigned long long head, unsigned long long n);
 
 int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf16(bool transcode);
