@@ -319,9 +319,120 @@ struct Utf16Codec {
   }
 };
 
+// Validation / lengths without barriers: warp rows of 1024 units in grid
+// stride, per-row counts for the error case (as utf8_validate_rows_kernel).
+constexpr int K16_ROW = 32 * K16_UPT;  // units per warp row
+
 template <bool kBE, bool kUnits = false>
-__global__ void __launch_bounds__(kComputeThreads, 4) utf16_validate_kernel(U16Args a) {
-  validate_body<Utf16Codec<kBE>, kUnits>(a);
+__global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) {
+  unsigned* const row_counts = a.rows;
+  __shared__ unsigned long long warp_tot[8];
+  __shared__ bool last;
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  const long long head = (long long)a.head, end = (long long)(a.head + a.n);
+  const unsigned long long nrows = (unsigned long long)(end + K16_ROW - 1) / K16_ROW;
+  const Src16 src{a.base, a.head, a.n, kBE};
+  unsigned long long total = 0;
+  unsigned it = 0;
+  for (unsigned long long row = gw; row < nrows; row += nwarps, it++) {
+    const long long r0 = (long long)row * K16_ROW;
+    if ((it & 3) == 0) {  // stop behind a known error (warp-uniform decision)
+      unsigned long long e = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
+      e = __shfl_sync(0xffffffffu, e, 0);
+      if (e != kNoError && (long long)e + head < r0) break;
+    }
+    const long long v0 = r0 + (long long)K16_UPT * lane;
+    const bool interior = r0 - 2 >= head && r0 + K16_ROW + 2 <= end;
+    Words16 W;
+    if (interior) {
+      const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const uint4 v = __ldg(p + r);
+        W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y;
+        W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
+      }
+      uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K16_WPT], 1);
+      uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
+      if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 2));
+      if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K16_UPT));
+      W.w[0] = pw;
+      W.w[K16_WPT + 1] = nw;
+      if (kBE) {
+#pragma unroll
+        for (int k = 0; k < K16_WPT + 2; k++) W.w[k] = prmt(W.w[k], 0, 0x2301);
+      }
+    } else {
+      load_masked16(src, v0, W);
+    }
+    const Class16 c = classify16(W);
+    unsigned cnt;
+    if (interior && !c.err) {
+      cnt = kUnits ? c.bytes : c.chars;
+    } else {
+      const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
+      const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
+      const unsigned er = first_error16(src, v0, lo, hi);
+      if (er != kNone16) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
+      cnt = generic_units(src, v0, lo, hi, kUnits, nullptr);
+    }
+    total += cnt;
+    const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) row_counts[row] = rc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0) warp_tot[wib] = total;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; w++) t += warp_tot[w];
+    if (t) atomicAdd(&a.ctl->count, t);
+    __threadfence();
+    last = atomicAdd(&a.ctl->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const unsigned long long e = load_relaxed(&a.ctl->err);
+  unsigned long long written = load_relaxed(&a.ctl->count);
+  if (e != kNoError) {
+    const unsigned long long erow = (e + a.head) / K16_ROW;
+    unsigned long long t = 0;
+    for (unsigned long long r = threadIdx.x; r < erow; r += blockDim.x)
+      t += ((volatile unsigned*)row_counts)[r];
+    if (wib == 0) {
+      const long long v0 = (long long)erow * K16_ROW + (long long)K16_UPT * lane;
+      const long long stop = (long long)e + head;
+      const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
+      const unsigned lim = (unsigned)max((long long)lo, min((long long)K16_UPT, stop - v0));
+      t += generic_units(src, v0, lo, lim, kUnits, nullptr);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) warp_tot[wib] = t;
+    __syncthreads();
+    written = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; w++) written += warp_tot[w];
+  }
+  if (threadIdx.x == 0) {
+    vt_result r;
+    r.written = written;
+    r.consumed = e == kNoError ? a.n : e;
+    r.error_at = e == kNoError ? -1 : (long long)e;
+    *a.res = r;
+    a.ctl->tile_counter = 0;
+    a.ctl->count = 0;
+    a.ctl->err = kNoError;
+    __threadfence();
+    a.ctl->done = 0;
+  }
+}
+
+unsigned rows_utf16(unsigned long long head, unsigned long long n) {
+  return (unsigned)((head + n + K16_ROW - 1) / K16_ROW);
 }
 
 // UTF-16LE (kBE = false) or UTF-16BE (kBE = true) -> UTF-8
@@ -352,11 +463,11 @@ int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s) {
   else if (mode == kModeTranscodeBE)
     utf16_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf16Codec<true>>), s>>>(a);
   else if (mode == kModeValidateBE)
-    utf16_validate_kernel<true><<<grid, kComputeThreads, 0, s>>>(a);
+    utf16_validate_rows_kernel<true><<<grid, 256, 0, s>>>(a);
   else if (mode == kModeLength)
-    utf16_validate_kernel<false, true><<<grid, kComputeThreads, 0, s>>>(a);
+    utf16_validate_rows_kernel<false, true><<<grid, 256, 0, s>>>(a);
   else
-    utf16_validate_kernel<false><<<grid, kComputeThreads, 0, s>>>(a);
+    utf16_validate_rows_kernel<false><<<grid, 256, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -367,7 +478,7 @@ int occupancy_utf16(bool transcode) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_transcode_kernel<false>, kPipeBlock,
                                                   sizeof(PipeSmem<Utf16Codec<false>>));
   } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_validate_kernel<false>, kComputeThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, utf16_validate_rows_kernel<false>, 256, 0);
   }
   return n;
 }

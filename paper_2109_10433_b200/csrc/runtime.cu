@@ -207,6 +207,12 @@ int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, ui
   a.base = reinterpret_cast<const uint16_t*>(p - (p & 15));
   a.n = n;
   a.ntiles = vt::tiles_utf16(a.head, n);
+  a.rows = nullptr;
+  if (!transcode) {
+    const unsigned rows = vt::rows_utf16(a.head, n);
+    VT_TRY(ensure_rows(*sc, s, rows));
+    a.rows = sc->rows;
+  }
   VT_TRY(prepare(*sc, s, a.ntiles, a.epoch));
   a.out = d_out;
   a.status = sc->status;

@@ -51,6 +51,7 @@ struct U16Args {
   unsigned long long* status;
   Ctl* ctl;
   vt_result* res;
+  unsigned* rows;  // validate only: per-row counts scratch (rows_utf16 entries)
 };
 
 // launch modes: validate/count, transcode to UTF-16LE / UTF-8, transcode to
@@ -68,6 +69,7 @@ unsigned rows_utf8(unsigned long long head, unsigned long long n);
 int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf16(bool transcode);
 unsigned tiles_utf16(unsigned long long head, unsigned long long n);
+unsigned rows_utf16(unsigned long long head, unsigned long long n);
 
 // Batched validation of many short strings (one warp per string).
 int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,

@@ -12,13 +12,12 @@
 //       through atomicMin(&ctl->err) and clipped out of the counts
 //   emit(a, tc, stage, off)  write this thread's output at stage + off
 //
-// Two kernels are built from it:
-//   validate_body: count only; the code-point total goes to ctl->count;
-//   transcode_body: warp-specialised.  Warps 0..7 count tile j, hand its
-//       aggregate to warp 8, decode tile j into staging buffer j%2 and copy
-//       tile j-1 to global memory once warp 8 has resolved its offset with
-//       the decoupled look-back.  The look-back latency hides behind a whole
-//       tile of work.  Tiles are taken in order, one at a time per CTA.
+// transcode_body is the kernel body: warp-specialised.  Warps 0..7 count tile
+// j and decode it into the staging buffer, then copy it to global memory during
+// tile j+1, once warp 8 has resolved its offset with the decoupled look-back
+// (started when tile j was taken).  Tiles are taken in order, one at a time per
+// CTA.  (Validation and lengths need no offsets and use the barrier-free row
+// kernels in k_utf8.cu / k_utf16.cu.)
 #pragma once
 
 #include "vt_device.cuh"
@@ -73,24 +72,6 @@ __device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems
   const unsigned long long e = load_relaxed(&a.ctl->err);
   if (t < a.ntiles && e != kNoError && (e + a.head) / tile_elems < t) t = a.ntiles;
   return t;
-}
-
-// kUnits: count output elements (the transcode's `written`) instead of code points.
-template <class C, bool kUnits = false>
-__device__ __forceinline__ void validate_body(const typename C::Args& a) {
-  __shared__ unsigned red[kComputeThreads / 32], scan[kComputeThreads / 32];
-  __shared__ unsigned tile_s;
-  while (true) {
-    if (threadIdx.x == 0) tile_s = grab_tile(a, C::kTileElems);
-    __syncthreads();
-    const unsigned tile = tile_s;
-    if (tile >= a.ntiles) break;
-    typename C::TileCount tc;
-    unsigned off, total;
-    C::template count<kUnits, kComputeThreads, SyncAll>(a, tile, red, scan, tc, off, total);
-    if (threadIdx.x == 0 && total) atomicAdd(&a.ctl->count, (unsigned long long)total);
-  }
-  finalize_if_last(a, false, C::kTileElems);
 }
 
 // Staging buffers per CTA: 2 would let tile j be decoded while tile j-1 is
