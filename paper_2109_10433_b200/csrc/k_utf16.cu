@@ -71,10 +71,11 @@ __device__ __noinline__ void load_masked16(Src16 a, long long v0, Words16& W) {
 __device__ __forceinline__ bool is_hi(unsigned u) { return (u & 0xFC00u) == 0xD800u; }
 __device__ __forceinline__ bool is_lo(unsigned u) { return (u & 0xFC00u) == 0xDC00u; }
 
-// UTF-8 bytes of the unit at position i (little-endian in the result) and
-// their number; `nx` is the unit after it.
-__device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned nx, unsigned& len) {
-  unsigned cp = u;
+// UTF-8 bytes written for the unit u (little-endian in the result) and their
+// number; `pv` is the unit before it.  A surrogate pair's 4 bytes are split
+// 2 + 2 between its halves (see emit_word16_swar), so each unit writes 1-3
+// bytes and a pair may straddle threads and tiles.
+__device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned pv, unsigned& len) {
   if (u < 0x80u) {
     len = 1;
     return u;
@@ -83,15 +84,14 @@ __device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned nx, unsigne
     len = 2;
     return 0x80C0u | (u >> 6) | ((u & 0x3Fu) << 8);
   }
-  if (is_lo(u)) {
-    len = 0;
-    return 0;
+  if (is_hi(u)) {  // code point bits 10..20: w = (u & 0x3FF) + 0x40
+    const unsigned w = (u & 0x3FFu) + 0x40u;
+    len = 2;
+    return (0xF0u | (w >> 8)) | ((0x80u | ((w >> 2) & 0x3Fu)) << 8);
   }
-  if (is_hi(u)) {
-    cp = 0x10000u + (((u & 0x3FFu) << 10) | (nx & 0x3FFu));
-    len = 4;
-    return 0x808080F0u | (cp >> 18) | (((cp >> 12) & 0x3Fu) << 8) | (((cp >> 6) & 0x3Fu) << 16) |
-           ((cp & 0x3Fu) << 24);
+  if (is_lo(u)) {  // (w & 3) == (pv & 3)
+    len = 2;
+    return (0x80u | ((pv & 3u) << 4) | ((u >> 6) & 0xFu)) | ((0x80u | (u & 0x3Fu)) << 8);
   }
   len = 3;
   return 0x8080E0u | (u >> 12) | (((u >> 6) & 0x3Fu) << 8) | ((u & 0x3Fu) << 16);
@@ -118,7 +118,7 @@ __device__ __noinline__ unsigned generic_units(Src16 a, long long v0, unsigned l
   for (unsigned i = lo; i < lim; i++) {
     const unsigned u = unit_at(W, (int)i);
     unsigned len;
-    const uint32_t p = encode_unit(u, unit_at(W, (int)i + 1), len);
+    const uint32_t p = encode_unit(u, unit_at(W, (int)i - 1), len);
     if (!bytes) {
       q += is_lo(u) ? 0u : 1u;
       continue;
@@ -152,7 +152,7 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
     lp = ~nz_hi6((x & 0xFC00FC00u) ^ 0xDC00DC00u) & H16;
   }
   uint32_t hcur = 0, lcur = 0;
-  uint32_t err = 0, acc = 0, nlo = 0;
+  uint32_t err = 0, acc = 0, nlo = 0, nsur = 0;
 #pragma unroll
   for (int k = 1; k <= K16_WPT + 1; k++) {
     const uint32_t x = W.w[k];
@@ -168,8 +168,9 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
     if (k <= K16_WPT) {
       const uint32_t g80 = ((((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16) >> 15;
       const uint32_t g800 = ((((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16) >> 15;
-      acc += g80 + g800 + (hm >> 15);
+      acc += g80 + g800;
       nlo += lm >> 15;
+      nsur += (hm | lm) >> 15;
       hcur = hm;
       lcur = lm;
     }
@@ -177,7 +178,9 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
   (void)lp;
   Class16 c;
   const unsigned a = (acc & 0xFFFFu) + (acc >> 16), l = (nlo & 0xFFFFu) + (nlo >> 16);
-  c.bytes = K16_UPT + a - 3 * l;
+  const unsigned sr = (nsur & 0xFFFFu) + (nsur >> 16);
+  // bytes per unit: 1 + [u >= 0x80] + [u >= 0x800] - [surrogate] (2 + 2 per pair)
+  c.bytes = K16_UPT + a - sr;
   c.chars = K16_UPT - l;
   c.err = err != 0;
   return c;
@@ -253,45 +256,54 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
-// Branch-free UTF-8 encoding of one unit u (followed by nx): the bytes,
-// little-endian, and their number (0 for the low half of a pair).
-__device__ __forceinline__ uint32_t encode_unit_bf(uint32_t u, uint32_t nx, uint32_t& len) {
-  const uint32_t g80 = u >= 0x80u, g800 = u >= 0x800u;
-  const uint32_t top6 = u >> 10;  // 0x36: high surrogate, 0x37: low surrogate
-  const uint32_t hs = top6 == 0x36u, ls = top6 == 0x37u;
-  // 2- and 3-byte forms (used for every BMP unit, selected by g800)
-  const uint32_t p2 = 0x80C0u | (u >> 6) | ((u << 8) & 0x3F00u);
-  const uint32_t p3 = 0x8080E0u | (u >> 12) | ((u << 2) & 0x3F00u) | ((u << 16) & 0x3F0000u);
-  // 4-byte form of the pair (u, nx)
-  const uint32_t cp = 0x10000u + (((u & 0x3FFu) << 10) | (nx & 0x3FFu));
-  const uint32_t p4 = 0x808080F0u | (cp >> 18) | ((cp >> 4) & 0x3F00u) | ((cp << 10) & 0x3F0000u) |
-                      ((cp << 24) & 0x3F000000u);
-  uint32_t p = g800 ? p3 : (g80 ? p2 : u);
-  p = hs ? p4 : p;
-  len = ls ? 0u : 1u + g80 + g800 + hs;
-  return p;
-}
-
-// Encode one word (two units) at the running shared address q.
-__device__ __forceinline__ void emit_word16(uint32_t x, uint32_t nxw, uint32_t& q) {
+// Both units of a word at once (16-bit SWAR lanes).  Every unit is written
+// as 1-3 bytes: BMP units as themselves; a surrogate pair's 4 bytes are split
+// 2 + 2 between its halves -- with w = (hi & 0x3FF) + 0x40 (code point bits
+// 10..20), the high half writes F0|w>>8, 80|(w>>2)&3F and the low half writes
+// 80|(w&3)<<4|(lo>>6)&0xF, 80|lo&3F, where w & 3 == hi & 3.  So no lane needs
+// its neighbour except for two bits of the previous unit.  px: previous word.
+__device__ __forceinline__ void emit_word16_swar(uint32_t x, uint32_t px, uint32_t& q) {
   if ((x & 0xFF80FF80u) == 0) {  // two ASCII units
     sts8(q, x);
     sts8(q + 1, x >> 16);
     q += 2;
     return;
   }
-#pragma unroll
-  for (int h = 0; h < 2; h++) {
-    const uint32_t u = h ? (x >> 16) : (x & 0xFFFFu);
-    const uint32_t nx = h ? (nxw & 0xFFFFu) : (x >> 16);
-    uint32_t len;
-    const uint32_t p = encode_unit_bf(u, nx, len);
-    if (len >= 1) sts8(q, p);
-    if (len >= 2) sts8(q + 1, p >> 8);
-    if (len >= 3) sts8(q + 2, p >> 16);
-    if (len >= 4) sts8(q + 3, p >> 24);
-    q += len;
-  }
+  const uint32_t g80 = (((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16;   // u >= 0x80
+  const uint32_t g800 = (((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16;  // u >= 0x800
+  const uint32_t sur = ~nz_hi6((x & 0xF800F800u) ^ 0xD800D800u) & H16;   // D800..DFFF
+  const uint32_t hs = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;    // D800..DBFF
+  const uint32_t is3 = g800 & ~sur;
+  // full 16-bit lane masks (PRMT sign replication of bytes 1 and 3)
+  const uint32_t m80 = prmt(g80, 0, 0xBB99), m3 = prmt(is3, 0, 0xBB99);
+  const uint32_t ms = prmt(sur, 0, 0xBB99), mh = prmt(hs, 0, 0xBB99);
+  const uint32_t c6 = x & 0x003F003Fu;
+  const uint32_t b6 = (x >> 6) & 0x003F003Fu;
+  const uint32_t a4 = (x >> 12) & 0x000F000Fu;
+  const uint32_t w = (x & 0x03FF03FFu) + 0x00400040u;
+  const uint32_t pu = __funnelshift_l(px, x, 16);  // previous unit of each lane
+  // first byte
+  const uint32_t f_lo = 0x00800080u | ((pu & 0x00030003u) << 4) | (b6 & 0x000F000Fu);
+  const uint32_t f_hi = 0x00F000F0u | (w >> 8);
+  const uint32_t f_sur = (f_hi & mh) | (f_lo & ~mh);
+  const uint32_t f_bmp = (m3 & (0x00E000E0u | a4)) | (~m3 & (0x00C000C0u | b6));
+  uint32_t F = (ms & f_sur) | (~ms & f_bmp);
+  F = (m80 & F) | (~m80 & x);
+  // second and third bytes
+  const uint32_t s_hi = (w >> 2) & 0x003F003Fu;
+  const uint32_t S = 0x00800080u | (m3 & b6) | (mh & s_hi) | (~(m3 | mh) & c6);
+  const uint32_t T = 0x00800080u | c6;
+  // per-lane length 1..3
+  const uint32_t n = 0x00010001u + (g80 >> 15) + (is3 >> 15);
+  const uint32_t n0 = n & 0xFFFFu, n1 = n >> 16;
+  sts8(q, F);
+  if (n0 >= 2) sts8(q + 1, S);
+  if (n0 == 3) sts8(q + 2, T);
+  q += n0;
+  sts8(q, F >> 16);
+  if (n1 >= 2) sts8(q + 1, S >> 16);
+  if (n1 == 3) sts8(q + 2, T >> 16);
+  q += n1;
 }
 
 template <bool kBE>
@@ -312,7 +324,7 @@ struct Utf16Codec {
     if (tc.simple) {
       uint32_t q = smem_addr(stage) + off;
 #pragma unroll
-      for (int k = 1; k <= K16_WPT; k++) emit_word16(tc.W.w[k], tc.W.w[k + 1], q);
+      for (int k = 1; k <= K16_WPT; k++) emit_word16_swar(tc.W.w[k], tc.W.w[k - 1], q);
     } else {
       generic_units(Src16{a.base, a.head, a.n, kBE}, tc.v0, tc.lo, tc.lim, true, stage + off);
     }
