@@ -37,6 +37,19 @@ __device__ __forceinline__ uint32_t nz_hi6(uint32_t v) {
   return ((v >> 1) + 0x7E007E00u) & H16;
 }
 
+// Per-lane unsigned compares u >= 0x80 / u >= 0x800 (bit 15 of each lane):
+// the low 15 bits plus a bias carry into bit 15, or bit 15 is already set.
+__device__ __forceinline__ uint32_t ge80_16(uint32_t x, uint32_t x15) {
+  return lop3<0xA8>(x15 + 0x7F807F80u, x, H16);  // (a | b) & c
+}
+__device__ __forceinline__ uint32_t ge800_16(uint32_t x, uint32_t x15) {
+  return lop3<0xA8>(x15 + 0x78007800u, x, H16);
+}
+// D800..DFFF lanes (bit 15)
+__device__ __forceinline__ uint32_t sur16(uint32_t x) {
+  return ~nz_hi6((x & 0xF800F800u) ^ 0xD800D800u) & H16;
+}
+
 struct Src16 {
   const uint16_t* base;
   unsigned long long head, n;
@@ -145,19 +158,18 @@ struct Class16 {
 
 // Phase A over the 16 own words: pairing check and counts (SWAR, 16-bit lanes).
 __device__ __forceinline__ Class16 classify16(const Words16& W) {
-  uint32_t hp, lp;  // surrogate planes of the previous word
+  uint32_t hp;  // high-surrogate plane of the previous word
   {
     const uint32_t x = W.w[0];
-    hp = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;
-    lp = ~nz_hi6((x & 0xFC00FC00u) ^ 0xDC00DC00u) & H16;
+    hp = sur16(x) & ~(x << 5);
   }
   uint32_t hcur = 0, lcur = 0;
   uint32_t err = 0, acc = 0, nlo = 0, nsur = 0;
 #pragma unroll
   for (int k = 1; k <= K16_WPT + 1; k++) {
     const uint32_t x = W.w[k];
-    const uint32_t hm = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;
-    const uint32_t lm = ~nz_hi6((x & 0xFC00FC00u) ^ 0xDC00DC00u) & H16;
+    const uint32_t sr = sur16(x), x5 = x << 5;  // bit 10 (low surrogate) -> bit 15
+    const uint32_t hm = sr & ~x5, lm = sr & x5;
     if (k >= 2) {
       // word k-1: its units' predecessors and successors
       const uint32_t prev_hi = __funnelshift_l(hp, hcur, 16);
@@ -166,21 +178,19 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
       hp = hcur;
     }
     if (k <= K16_WPT) {
-      const uint32_t g80 = ((((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16) >> 15;
-      const uint32_t g800 = ((((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16) >> 15;
-      acc += g80 + g800;
+      const uint32_t x15 = x & 0x7FFF7FFFu;
+      acc += (ge80_16(x, x15) >> 15) + (ge800_16(x, x15) >> 15);
       nlo += lm >> 15;
-      nsur += (hm | lm) >> 15;
+      nsur += sr >> 15;
       hcur = hm;
       lcur = lm;
     }
   }
-  (void)lp;
   Class16 c;
   const unsigned a = (acc & 0xFFFFu) + (acc >> 16), l = (nlo & 0xFFFFu) + (nlo >> 16);
-  const unsigned sr = (nsur & 0xFFFFu) + (nsur >> 16);
+  const unsigned sn = (nsur & 0xFFFFu) + (nsur >> 16);
   // bytes per unit: 1 + [u >= 0x80] + [u >= 0x800] - [surrogate] (2 + 2 per pair)
-  c.bytes = K16_UPT + a - sr;
+  c.bytes = K16_UPT + a - sn;
   c.chars = K16_UPT - l;
   c.err = err != 0;
   return c;
@@ -269,6 +279,7 @@ __device__ __forceinline__ void emit_word16_swar(uint32_t x, uint32_t px, uint32
     q += 2;
     return;
   }
+  // (the shared-plane forms of classify16 spill here: measured slower)
   const uint32_t g80 = (((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16;   // u >= 0x80
   const uint32_t g800 = (((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16;  // u >= 0x800
   const uint32_t sur = ~nz_hi6((x & 0xF800F800u) ^ 0xD800D800u) & H16;   // D800..DFFF
