@@ -376,9 +376,10 @@ def main():
             line["roofline"]["traffic"] = t["dram_bytes_per_launch"]
             line["roofline"]["traffic_source"] = t["source"]
 
-    if rank == 0 and world == 1 and not args.no_e2e and kind != "rt":
+    if not args.no_e2e and kind != "rt":
         # end to end through the drop-in (host-pointer) C ABI: pinned host input,
-        # H2D + kernel + D2H of result and output inside the timed region
+        # H2D + kernel + D2H of result and output inside the timed region; every
+        # rank on its own slice, the slowest rank's time for the whole job
         import ctypes
 
         L = vt.lib()
@@ -400,15 +401,27 @@ def main():
         for _ in range(2):
             e2e_step()
         k = max(3, min(args.steps, 10))
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(k):
             e2e_step()
         dt = (time.perf_counter() - t0) / k
         assert r.written == res.written and r.error_at == (-1 if res.error_at is None else res.error_at)
-        line["e2e"] = {"value": round(in_bytes / dt / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": in_bytes,
-                       "d2h_bytes_per_step": elem_out * int(r.written) + 24,
-                       "api": f"{fn.__name__} (drop-in boundary), pinned host buffers",
-                       "ms_per_step": round(dt * 1e3, 3)}
+        d2h = elem_out * int(r.written) + 24
+        if dist:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+            b = torch.tensor([d2h], dtype=torch.int64, device="cuda")
+            dist.all_reduce(b)
+            d2h = int(b.item())
+        if rank == 0:
+            line["e2e"] = {"value": round(total_in / dt / 1e9, 3), "unit": "GB/s",
+                           "h2d_bytes_per_step": total_in, "d2h_bytes_per_step": d2h,
+                           "api": f"{fn.__name__} (drop-in boundary), pinned host buffers"
+                                  + (f", {world} ranks, max over ranks" if world > 1 else ""),
+                           "ms_per_step": round(dt * 1e3, 3)}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ckind = "u16" if kind == "u16" else "u8"
