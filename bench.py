@@ -325,10 +325,11 @@ def main():
     per_step_ms = ms_max / args.steps
     if kind == "u16":
         chars = vt.validate_utf16_device(d_in, n).written
-        alg_bytes = 2 * n + res.written
+        # a call that stops at an error only has to read up to it
+        alg_bytes = 2 * (n if res.error_at is None else res.error_at) + res.written
     elif kind == "u8":
         chars = vt.validate_utf8_device(d_in, n).written
-        alg_bytes = n + 2 * res.written
+        alg_bytes = (n if res.error_at is None else res.error_at) + 2 * res.written
     else:
         chars = vt.validate_utf8_device(d_in, n).written
         alg_bytes = 2 * n + 4 * res.written  # 8->16 (n + 2 u16) + 16->8 (2 u16 + n)
@@ -403,22 +404,25 @@ def main():
         k = max(3, min(args.steps, 10))
         if dist:
             dist.barrier()
+        x0 = vt.host_transfer_counts()
         t0 = time.perf_counter()
         for _ in range(k):
             e2e_step()
         dt = (time.perf_counter() - t0) / k
+        x1 = vt.host_transfer_counts()
         assert r.written == res.written and r.error_at == (-1 if res.error_at is None else res.error_at)
-        d2h = elem_out * int(r.written) + 24
+        # bytes actually moved per step (a call stops early behind an error)
+        h2d, d2h = (x1[0] - x0[0]) // k, (x1[1] - x0[1]) // k
         if dist:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-            b = torch.tensor([d2h], dtype=torch.int64, device="cuda")
+            b = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
             dist.all_reduce(b)
-            d2h = int(b.item())
+            h2d, d2h = int(b[0].item()), int(b[1].item())
         if rank == 0:
             line["e2e"] = {"value": round(total_in / dt / 1e9, 3), "unit": "GB/s",
-                           "h2d_bytes_per_step": total_in, "d2h_bytes_per_step": d2h,
+                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                            "api": f"{fn.__name__} (drop-in boundary), pinned host buffers"
                                   + (f", {world} ranks, max over ranks" if world > 1 else ""),
                            "ms_per_step": round(dt * 1e3, 3)}

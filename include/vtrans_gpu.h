@@ -203,6 +203,10 @@ const char* vt_status_string(int status);
 int vt_device_count(void);
 /* Number of kernels this library launched so far in the calling process. */
 uint64_t vt_launch_count(void);
+/* Cumulative host<->device bytes moved by the calling thread's vt_host_*
+ * transcoding calls (pipelined copies, or mapped-memory traffic of the
+ * zero-copy path), for end-to-end accounting. */
+void vt_host_transfer_counts(uint64_t* h2d, uint64_t* d2h);
 const char* vt_build_info(void);
 
 #ifdef __cplusplus

@@ -129,6 +129,7 @@ def lib():
         "vt_status_string": (C.c_char_p, [C.c_int]),
         "vt_device_count": (C.c_int, []),
         "vt_launch_count": (C.c_uint64, []),
+        "vt_host_transfer_counts": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "vt_build_info": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -524,6 +525,13 @@ def utf8_class_counts(data) -> Optional[tuple[int, int, int, int]]:
     _check(lib().vt_host_utf8_class_counts(_ptr(a), len(a), C.byref(counts), C.byref(valid)),
            "utf8_class_counts")
     return tuple(int(x) for x in counts) if valid.value else None
+
+
+def host_transfer_counts() -> tuple[int, int]:
+    """(H2D, D2H) bytes moved so far by this thread's host-pointer transcoding calls."""
+    a, b = C.c_uint64(), C.c_uint64()
+    lib().vt_host_transfer_counts(C.byref(a), C.byref(b))
+    return int(a.value), int(b.value)
 
 
 def launch_count() -> int:

@@ -308,6 +308,9 @@ struct HostCtx {
 };
 
 thread_local std::map<int, HostCtx> t_ctx;
+// bytes moved host<->device by this thread's host-pointer calls (copies, and
+// mapped-memory reads/writes of the zero-copy path)
+thread_local uint64_t t_h2d = 0, t_d2h = 0;
 
 int host_ctx(HostCtx*& out) {
   int dev;
@@ -428,6 +431,8 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
       src = reinterpret_cast<const In*>(c->ph_in[b]);
     }
     VT_TRY(cudaMemcpyAsync(c->pd_in[b], src, len * sizeof(In), cudaMemcpyHostToDevice, s));
+    t_h2d += len * sizeof(In);
+    t_d2h += sizeof(vt_result);
     VT_TRY(run(reinterpret_cast<const In*>(c->pd_in[b]), len, reinterpret_cast<Out*>(c->pd_out[b]),
                c->pd_res + b, s));
     VT_TRY(cudaMemcpyAsync(c->ph_res + b, c->pd_res + b, sizeof(vt_result),
@@ -445,6 +450,7 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
     VT_TRY(cudaEventSynchronize(c->pev[b]));
     const vt_result r = c->ph_res[b];
     if (written + r.written > out_cap_elems) return VT_E_ARG;
+    t_d2h += r.written * sizeof(Out);
     if (r.written) {
       if (pin_out) {
         VT_TRY(cudaMemcpyAsync(out + written, c->pd_out[b], r.written * sizeof(Out),
@@ -491,6 +497,8 @@ int host_transcode(const In* in, uint64_t n, Out* out, uint64_t out_cap_elems, v
     VT_TRY(run(din, n, dout, dres, c->stream));
     VT_TRY(cudaStreamSynchronize(c->stream));
     *res = *c->h_res;
+    t_h2d += in_bytes;
+    t_d2h += res->written * sizeof(Out) + sizeof(vt_result);
     if (res->written > out_cap_elems) return VT_E_ARG;
     if (res->written) std::memcpy(out, c->h_out, res->written * sizeof(Out));
     return 0;
@@ -1107,6 +1115,11 @@ int vt_host_utf8_class_counts(const uint8_t* in, uint64_t n, uint64_t counts[4],
   }
   for (int i = 0; i < 4; i++) counts[i] = c->h_counts[i];
   return 0;
+}
+
+void vt_host_transfer_counts(uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = t_h2d;
+  if (d2h) *d2h = t_d2h;
 }
 
 }  // extern "C"
