@@ -156,21 +156,33 @@ def test_errors_at_seams(oracle):
                 out, r = vt.utf8_to_utf16(data)
                 assert _same(r, want), (ctx, seam, b.hex())
                 assert np.array_equal(out, want_out)
+                assert vt.first_error_utf8(data) == want.error_at  # validate kernel (warp rows)
+                assert vt.utf16_len_from_utf8(data) is None
 
 
 def test_utf16_pairs_across_seams(oracle):
-    for seam in [1, 7, 8, 9, 2047, 2048, 2049, 4095, 4096, 4097, 8191, 8192]:
-        for mode in range(3):
-            u = np.full(12000, 0x93E1, dtype=np.uint16)
-            u[seam - 1], u[seam] = 0xD83D, 0xDE00
-            if mode == 1:
-                u[seam] = 0x0041  # unpaired high
-            if mode == 2:
-                u[seam - 1] = 0x0041  # lone low
-            want_out, want = oracle.utf16_to_utf8(u)
-            out, r = vt.utf16_to_utf8(u)
-            assert _same(r, want) and np.array_equal(out, want_out), (seam, mode)
-            assert vt.validate_utf16(u) == oracle.validate_utf16(u)
+    """Surrogate pairs (written 2 + 2 bytes by their halves) and broken pairs at
+    every kind of seam: words (2 units), threads (32), warp rows (1024), tiles
+    (8192), in ASCII, 2-byte and 3-byte context."""
+    seams = [1, 2, 3, 31, 32, 33, 63, 64, 65, 1023, 1024, 1025, 2047, 2048, 4095, 4096,
+             8191, 8192, 8193, 16383, 16384]
+    for fill in (0x0061, 0x00E9, 0x93E1):
+        for seam in seams:
+            for mode in range(4):
+                u = np.full(20000, fill, dtype=np.uint16)
+                u[seam - 1], u[seam] = 0xD83D, 0xDE00
+                if mode == 1:
+                    u[seam] = 0x0041  # unpaired high
+                if mode == 2:
+                    u[seam - 1] = 0x0041  # lone low
+                if mode == 3 and seam + 2 < len(u):  # two pairs back to back
+                    u[seam + 1], u[seam + 2] = 0xDBFF, 0xDFFF
+                want_out, want = oracle.utf16_to_utf8(u)
+                out, r = vt.utf16_to_utf8(u)
+                assert _same(r, want) and np.array_equal(out, want_out), (fill, seam, mode)
+                assert vt.validate_utf16(u) == oracle.validate_utf16(u)
+                if mode == 0:
+                    assert vt.utf8_len_from_utf16(u) == want.written
 
 
 # ---- differential fuzz (cf. proj/src/harness.cpp:388-436) ---------------------------
