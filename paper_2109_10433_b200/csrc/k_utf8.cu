@@ -386,7 +386,9 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
                                           unsigned off) {
   if (tc.simple) {
     uint32_t q = smem_addr(stage) + 2u * off;
-    if (!tc.four) {
+    // warp-uniform choice (the 4-byte-capable form handles every word): a
+    // per-thread choice would run both forms in mixed warps
+    if (!__any_sync(0xffffffffu, tc.four)) {
 #pragma unroll
       for (int k = 1; k <= K8_WPT; k++) emit_word<false, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
