@@ -105,17 +105,6 @@ struct ClassOut {
   bool four;       // a 4-byte lead (or F8..FF) in our bytes
 };
 
-// Exact range check of the leads flagged in m (bit 7 of each lane) of word x,
-// followed by word nx; true if one of them does not decode.
-__device__ __forceinline__ bool lanes_fail(uint32_t m, uint32_t x, uint32_t nx) {
-  bool bad = false;
-  while (m) {
-    const unsigned lanebit = __ffs(m) - 1;  // 7, 15, 23 or 31
-    m &= m - 1;
-    if (!decode_ok(__funnelshift_r(x, nx, lanebit - 7))) bad = true;
-  }
-  return bad;
-}
 
 // Continuation requirements of the lead planes of one word as a 64-bit sum:
 // lane i+1 (l2), i+2 (l3), i+3 (l4); the high half belongs to the next word.
@@ -139,19 +128,27 @@ __device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint3
   return lop3<0xBA>(l2, ge_c2, h);                     // (a & ~b) | c: + C0 C1
 }
 
-// Exact range check of the special leads of every word (only threads whose
-// bytes contain such a lead get here; registers only).
-__device__ __forceinline__ bool specials_fail(const Words& W) {
-  bool bad = false;
+// Exact range check of the special leads of every word, for the threads the
+// filter flagged; out of line (inlining it costs the hot path registers) and
+// branch-free.  With the structure already checked, the only range errors are
+// on the lead and the byte after it (C0 C1; E0 + 80..9F; ED + A0..BF;
+// F0 + 80..8F; F4 + 90..BF; F5..FF): all lanes of a word at once.
+__device__ __noinline__ bool specials_fail(const Words W) {
+  uint32_t bad = 0;
 #pragma unroll
   for (int k = 1; k <= K8_WPT; k++) {
     const uint32_t x = W.w[k], x2 = x << 1;
-    const uint32_t l2 = x & x2 & H;
-    const uint32_t l3 = l2 & (x << 2);
-    const uint32_t m = special_lanes(x, l2, l3) & H;
-    if (m && lanes_fail(m, x, W.w[k + 1])) bad = true;
+    const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
+    const uint32_t x7 = x & 0x7F7F7F7Fu;
+    const uint32_t ge_c2 = x7 + 0x3E3E3E3Eu, ge_e1 = x7 + 0x1F1F1F1Fu;
+    const uint32_t ge_ed = x7 + 0x13131313u, ge_ee = x7 + 0x12121212u;
+    const uint32_t ge_f1 = x7 + 0x0F0F0F0Fu, ge_f4 = x7 + 0x0C0C0C0Cu, ge_f5 = x7 + 0x0B0B0B0Bu;
+    const uint32_t n1 = prmt(x, W.w[k + 1], 0x4321);  // byte i = the byte after it
+    const uint32_t b5 = n1 << 2, b45 = (n1 | (n1 << 1)) << 2;  // bit 7: n1 >= A0 / >= 90
+    bad |= (l2 & ~ge_c2) | (l3 & ~ge_e1 & ~b5) | (l3 & ge_ed & ~ge_ee & b5) |
+           (l4 & ~ge_f1 & ~b45) | (l4 & ge_f4 & ~ge_f5 & b45) | (l4 & ge_f5);
   }
-  return bad;
+  return (bad & H) != 0;
 }
 
 // Phase A over the 16 own words (SWAR, branch-free): structure check,
