@@ -114,17 +114,17 @@ __device__ __forceinline__ unsigned long long need_plane(uint32_t l2, uint32_t l
 }
 
 // Leads whose value range depends on the next byte, as bit 7 of each lane:
-// C0 C1, E0 ED (+ EE EF, harmless extras), F0 and F4..FF (F5..FF are always
-// invalid).  Per-lane unsigned compares x >= K on the low 7 bits (all leads
+// C0 C1, E0, ED..FF (EE EF and F1..F3 are harmless extras, checked exactly like
+// the rest).  Per-lane unsigned compares x >= K on the low 7 bits (all leads
 // have bit 7 set; no carry crosses a lane): the adds run on the FMA pipe
-// (VIADD), the three selections are single LOP3s.
+// (VIADD), the selections are single LOP3s.
 __device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint32_t l3) {
   const uint32_t x7 = x & 0x7F7F7F7Fu;
   const uint32_t ge_c2 = x7 + 0x3E3E3E3Eu, ge_e1 = x7 + 0x1F1F1F1Fu;
-  const uint32_t ge_ed = x7 + 0x13131313u, ge_f1 = x7 + 0x0F0F0F0Fu;
-  const uint32_t ge_f4 = x7 + 0x0C0C0C0Cu;
-  const uint32_t g = lop3<0xBA>(ge_ed, ge_f1, ge_f4);  // (a & ~b) | c: ED..F0, F4..FF
-  const uint32_t h = lop3<0xA2>(g, ge_e1, l3);         // (a | ~b) & c: 3/4-byte specials
+  const uint32_t ge_ed = x7 + 0x13131313u;
+  // (excluding F1..F3 as well costs two more ops per word and saves nothing:
+  // a warp with any flagged lane runs the exact check anyway)
+  const uint32_t h = lop3<0xA2>(ge_ed, ge_e1, l3);     // (a | ~b) & c: E0, ED..FF
   return lop3<0xBA>(l2, ge_c2, h);                     // (a & ~b) | c: + C0 C1
 }
 
