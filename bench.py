@@ -369,6 +369,25 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if kind in ("u8", "u16"):
+        # validation-only throughput on the same input (read-only,
+        # algorithmic bytes = the input), device-timed like the main number
+        vfn = vt.validate_utf16_device if kind == "u16" else vt.validate_utf8_device
+        vres = torch.zeros(3, dtype=torch.int64, device="cuda")
+        for _ in range(3):
+            vfn(d_in, n, stream=stream, d_res=vres)
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(args.steps):
+            vfn(d_in, n, stream=stream, d_res=vres)
+        v1.record(stream)
+        torch.cuda.synchronize()
+        vms = v0.elapsed_time(v1) / args.steps
+        vbytes = in_bytes if res.error_at is None else (2 if kind == "u16" else 1) * res.error_at
+        line["validate"] = {"kernel": "vt::utf16_validate_rows_kernel" if kind == "u16"
+                            else "vt::utf8_validate_rows_kernel",
+                            "ms_per_step": round(vms, 4), "input_gbs": round(in_bytes / vms / 1e6, 1),
+                            "roofline_frac": round(vbytes / vms / 1e6 / peak, 4)}
     tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr):
         with open(tr) as f:
