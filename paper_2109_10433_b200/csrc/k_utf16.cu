@@ -273,12 +273,8 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
 // 80|(w&3)<<4|(lo>>6)&0xF, 80|lo&3F, where w & 3 == hi & 3.  So no lane needs
 // its neighbour except for two bits of the previous unit.  px: previous word.
 __device__ __forceinline__ void emit_word16_swar(uint32_t x, uint32_t px, uint32_t& q) {
-  if ((x & 0xFF80FF80u) == 0) {  // two ASCII units
-    sts8(q, x);
-    sts8(q + 1, x >> 16);
-    q += 2;
-    return;
-  }
+  // (no ASCII-pair shortcut: in mixed warps it runs beside the full form;
+  // measured slower even on 90 % ASCII)
   // (the shared-plane forms of classify16 spill here: measured slower)
   const uint32_t g80 = (((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16;   // u >= 0x80
   const uint32_t g800 = (((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16;  // u >= 0x800

@@ -51,7 +51,8 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 #endif
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)(v & 0xFF)));
+  // stores the low byte of v (no masking instruction needed)
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
