@@ -313,12 +313,85 @@ __device__ __forceinline__ void emit_word16_swar(uint32_t x, uint32_t px, uint32
   q += n1;
 }
 
+// Same bytes as emit_word16_swar, with fewer ALU-pipe instructions (the kernel
+// is bound by the ALU pipe; IMAD and IADD go to the FMA pipe):
+//  * only the low byte of each 16-bit lane has to be right (sts8 stores the
+//    low byte), so most masks after right shifts disappear;
+//  * the surrogate test is one masked XOR and a carry (no shift);
+//  * kOverlap: all three bytes of both units are stored unconditionally and q
+//    advances by the real lengths -- a unit's unused S/T bytes land where the
+//    next unit's bytes go and are overwritten by them (same thread, program
+//    order).  Only the thread's last word may not spill (the bytes after it
+//    belong to the next thread): it takes the predicated form.
+template <bool kOverlap>
+__device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t& q) {
+  // (x15 through an asm LOP3: classify16 computes the same compare planes, and
+  // if the compiler shares them they stay live across the scan and spill)
+  const uint32_t x15 = lop3<0xC0>(x, 0x7FFF7FFFu, 0u);
+  const uint32_t g80 = lop3<0xA8>(x15 + 0x7F807F80u, x, H16);    // u >= 0x80
+  const uint32_t g800 = lop3<0xA8>(x15 + 0x78007800u, x, H16);   // u >= 0x800
+  // D800..DFFF: bit 15 set and bits 11..14 == 1011
+  const uint32_t t = (x & 0x78007800u) ^ 0x58005800u;
+  const uint32_t sur = lop3<0x20>(x, t + 0x78007800u, H16);       // a & ~b & c
+  const uint32_t hs = sur & ~(x * 32u);                           // bit 10 clear: high
+  const uint32_t is3 = g800 & ~sur;
+  const uint32_t m80 = prmt(g80, 0, 0xBB99), m3 = prmt(is3, 0, 0xBB99);
+  const uint32_t ms = prmt(sur, 0, 0xBB99), mh = prmt(hs, 0, 0xBB99);
+  // lengths 1 + [u >= 0x80] + [3-byte BMP]: a pair's halves write 2 + 2
+  const uint32_t n = 0x00010001u + (g80 >> 15) + (is3 >> 15);
+  const uint32_t q1 = q + (n & 0xFFFFu);
+  const uint32_t x6 = x >> 6;                                     // low byte: u bits 6..13
+  // first byte: ASCII u; 2-byte C0 | u>>6 (u < 0x800: bits 11..13 are 0);
+  // 3-byte E0 | u>>12; high surrogate F0 | w>>8; low surrogate 80 | (w&3)<<4 | (u>>6)&F
+  const uint32_t w = (x & 0x03FF03FFu) + 0x00400040u;              // code point bits 10..20
+  uint32_t F1;
+  {
+    const uint32_t F2 = x6 | 0x00C000C0u;
+    const uint32_t F3 = ((x >> 12) & 0x000F000Fu) | 0x00E000E0u;
+    const uint32_t Fh = (w >> 8) | 0x00F000F0u;
+    const uint32_t pu16 = prmt(px, x, 0x5432) * 16u;                // previous unit << 4
+    const uint32_t Fl = (lop3<0xCA>(0x000F000Fu, x6, pu16) & 0x003F003Fu) | 0x00800080u;
+    // selections (mux(m, a, b) = m ? a : b, LOP3 0xCA with the mask first)
+    const uint32_t Fn = lop3<0xCA>(ms, lop3<0xCA>(mh, Fh, Fl), lop3<0xCA>(m3, F3, F2));
+    const uint32_t F = lop3<0xCA>(m80, Fn, x);
+    sts8(q, F);
+    F1 = F >> 16;
+  }
+  const uint32_t T = (x & 0x003F003Fu) | 0x00800080u;
+  const uint32_t S3 = (x6 & 0x003F003Fu) | 0x00800080u;
+  const uint32_t Sh = ((w >> 2) & 0x003F003Fu) | 0x00800080u;
+  const uint32_t S = lop3<0xCA>(m3, S3, lop3<0xCA>(mh, Sh, T));
+  if (kOverlap) {
+    sts8(q + 1, S);
+    sts8(q + 2, T);
+    sts8(q1, F1);
+    sts8(q1 + 1, S >> 16);
+    sts8(q1 + 2, T >> 16);
+  } else {
+    const uint32_t n0 = n & 0xFFFFu, n1 = n >> 16;
+    if (n0 >= 2) sts8(q + 1, S);
+    if (n0 == 3) sts8(q + 2, T);
+    sts8(q1, F1);
+    if (n1 >= 2) sts8(q1 + 1, S >> 16);
+    if (n1 == 3) sts8(q1 + 2, T >> 16);
+  }
+  q = q1 + (n >> 16);
+}
+
+#ifndef VT_U16_EMIT
+#define VT_U16_EMIT 3
+#endif
+#ifndef VT_NSTAGE16
+#define VT_NSTAGE16 1  // two buffers: 1.375 vs 1.370 ms on cfg3 (with the L1 they take away)
+#endif
+
 template <bool kBE>
 struct Utf16Codec {
   using Args = U16Args;
   using TileCount = TileCount16;
   static constexpr int kTileElems = K16_TILE;
   static constexpr int kStageBytes = 3 * K16_TILE;
+  static constexpr int kNStage = VT_NSTAGE16;
   static constexpr int kOutBytes = 1;
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
@@ -330,8 +403,14 @@ struct Utf16Codec {
                                               unsigned off) {
     if (tc.simple) {
       uint32_t q = smem_addr(stage) + off;
+#if VT_U16_EMIT == 3
+#pragma unroll
+      for (int k = 1; k < K16_WPT; k++) emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q);
+      emit_word16_v3<false>(tc.W.w[K16_WPT], tc.W.w[K16_WPT - 1], q);
+#else
 #pragma unroll
       for (int k = 1; k <= K16_WPT; k++) emit_word16_swar(tc.W.w[k], tc.W.w[k - 1], q);
+#endif
     } else {
       generic_units(Src16{a.base, a.head, a.n, kBE}, tc.v0, tc.lo, tc.lim, true, stage + off);
     }
@@ -465,13 +544,16 @@ __global__ void __launch_bounds__(kPipeBlock, VT_K16_MINB) utf16_transcode_kerne
 }
 
 static int set_smem_attr16() {
-  int rc = (int)cudaFuncSetAttribute(utf16_transcode_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     sizeof(PipeSmem<Utf16Codec<false>>));
-  if (rc) return rc;
-  return (int)cudaFuncSetAttribute(utf16_transcode_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   sizeof(PipeSmem<Utf16Codec<true>>));
+  // (no carveout preference: forcing the largest shared-memory carveout
+  // leaves too little L1 for the input loads -- measured 1.37 vs 1.32 ms on
+  // cfg3)
+  for (const void* f :
+       {(const void*)utf16_transcode_kernel<false>, (const void*)utf16_transcode_kernel<true>}) {
+    const int rc = (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sizeof(PipeSmem<Utf16Codec<false>>));
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s) {
@@ -501,6 +583,12 @@ int occupancy_utf16(bool transcode) {
   }
   return n;
 }
+
+#ifdef VT_PHASES
+int read_phases16(unsigned long long* out8) {
+  return (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+}
+#endif
 
 unsigned tiles_utf16(unsigned long long head, unsigned long long n) {
   const unsigned long long t = (head + n + K16_TILE - 1) / K16_TILE;

@@ -397,12 +397,17 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
   }
 }
 
+#ifndef VT_NSTAGE8
+#define VT_NSTAGE8 1
+#endif
+
 template <bool kBE>
 struct Utf8Codec {
   using Args = U8Args;
   using TileCount = vt::TileCount;
   static constexpr int kTileElems = K8_TILE;
   static constexpr int kStageBytes = 2 * K8_TILE;
+  static constexpr int kNStage = VT_NSTAGE8;
   static constexpr int kOutBytes = 2;
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
@@ -560,13 +565,15 @@ __global__ void __launch_bounds__(kPipeBlock, VT_K8_MINB) utf8_transcode_kernel(
 }
 
 static int set_smem_attr() {
-  int rc = (int)cudaFuncSetAttribute(utf8_transcode_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     sizeof(PipeSmem<Utf8Codec<false>>));
-  if (rc) return rc;
-  return (int)cudaFuncSetAttribute(utf8_transcode_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   sizeof(PipeSmem<Utf8Codec<true>>));
+  // (no carveout preference: forcing the largest shared-memory carveout
+  // leaves too little L1 for the input loads -- measured 1.37 vs 1.32 ms on
+  // cfg3)
+  for (const void* f : {(const void*)utf8_transcode_kernel<false>, (const void*)utf8_transcode_kernel<true>}) {
+    const int rc = (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   sizeof(PipeSmem<Utf8Codec<false>>));
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s) {
@@ -594,6 +601,12 @@ int occupancy_utf8(bool transcode) {
   }
   return n;
 }
+
+#ifdef VT_PHASES
+int read_phases(unsigned long long* out8) {
+  return (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+}
+#endif
 
 unsigned tiles_utf8(unsigned long long head, unsigned long long n) {
   const unsigned long long t = (head + n + K8_TILE - 1) / K8_TILE;

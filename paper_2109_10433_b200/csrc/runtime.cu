@@ -22,6 +22,12 @@
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
+#ifdef VT_PHASES
+namespace vt {
+int read_phases(unsigned long long* out8);
+int read_phases16(unsigned long long* out8);
+}  // namespace vt
+#endif
 extern "C" uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut);
 extern "C" uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut);
 
@@ -71,6 +77,9 @@ int device_info(int dev, DeviceInfo& out) {
   d.occ_u8[1] = std::max(1, vt::occupancy_utf8(true));
   d.occ_u16[0] = std::max(1, vt::occupancy_utf16(false));
   d.occ_u16[1] = std::max(1, vt::occupancy_utf16(true));
+  if (std::getenv("VT_PRINT_OCC"))
+    std::fprintf(stderr, "vtrans: CTAs/SM utf8 validate %d transcode %d, utf16 validate %d transcode %d\n",
+                 d.occ_u8[0], d.occ_u8[1], d.occ_u16[0], d.occ_u16[1]);
   d.ok = true;
   g_devs[dev] = d;
   out = d;
@@ -1019,6 +1028,13 @@ int vt_debug_probe(vt_stream stream, uint64_t* out5) {
   VT_TRY(cudaMemcpy(out5, sc->ctl->pad, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return 0;
 }
+
+#ifdef VT_PHASES
+int vt_debug_phases(int utf16, uint64_t* out8) {
+  return utf16 ? vt::read_phases16(reinterpret_cast<unsigned long long*>(out8))
+               : vt::read_phases(reinterpret_cast<unsigned long long*>(out8));
+}
+#endif
 
 const char* vt_build_info(void) {
   return "libvtrans_gpu sm_100a (nvcc " VT_STR(__CUDACC_VER_MAJOR__) "." VT_STR(

@@ -220,11 +220,11 @@ template <int WS>
 __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_t sbase,
                                             unsigned mis, unsigned len, unsigned bs,
                                             unsigned nthreads) {
-  const unsigned nchunks = (mis + len + 15) >> 4;
   const unsigned end = mis + len;
-  // the first chunk may start before dst (mis != 0) and the last may end after
-  // it: those two go byte by byte, the rest with one 16-byte store
-  for (unsigned c = threadIdx.x; c < nchunks; c += nthreads) {
+  const unsigned c_end = end >> 4;  // chunks [mis ? 1 : 0, c_end) are whole
+  // whole chunks: two independent iterations per step (more stores in flight)
+#pragma unroll 2
+  for (unsigned c = (mis ? 1u : 0u) + threadIdx.x; c < c_end; c += nthreads) {
     const uint32_t a = sbase + 16u * c - (mis ? 16u : 0u);
     uint32_t x[8];
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -236,16 +236,19 @@ __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_
     v.y = __funnelshift_r(x[WS + 1], x[WS + 2], bs);
     v.z = __funnelshift_r(x[WS + 2], x[WS + 3], bs);
     v.w = __funnelshift_r(x[WS + 3], x[WS + 4], bs);
-    uint8_t* d = dbase + 16 * c;
-    if ((c > 0 || mis == 0) && 16 * c + 16 <= end) {
-      *reinterpret_cast<uint4*>(d) = v;
-    } else {
-      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int b = 0; b < 16; b++) {
-        const unsigned pos = 16 * c + b;  // relative to dbase
-        if (pos >= mis && pos < end) d[b] = (uint8_t)(vv[b >> 2] >> ((b & 3) * 8));
-      }
+    *reinterpret_cast<uint4*>(dbase + 16 * c) = v;
+  }
+  // the partial first chunk (bytes [mis, 16)) and last chunk (bytes
+  // [16 c_end, end)): one byte per thread, threads 0..15 and 16..31
+  const unsigned t = threadIdx.x;
+  if (t < 32) {
+    const unsigned pos = t < 16 ? t : 16u * c_end + (t - 16);
+    const bool first = t < 16 && mis != 0;
+    const bool last = t >= 16 && (end & 15u) != 0 && (c_end > 0 || mis == 0);
+    if ((first || last) && pos >= mis && pos < end) {
+      uint32_t b;
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(sbase + pos - mis));
+      dbase[pos] = (uint8_t)b;
     }
   }
 }

@@ -6,6 +6,7 @@
 //   kTileElems  input elements (bytes / units) per tile
 //   kStageBytes largest output of one tile, in bytes
 //   kOutBytes   bytes per output element (2 for UTF-16, 1 for UTF-8)
+//   kNStage     staging buffers per CTA (1 or 2, see PipeSmem)
 //   count<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg)
 //       load + validate + count the tile; off = this thread's exclusive
 //       output offset, agg = the tile's output (elements); errors reported
@@ -74,26 +75,26 @@ __device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems
   return t;
 }
 
-// Staging buffers per CTA: 2 would let tile j be decoded while tile j-1 is
-// still being copied out; 1 halves the shared memory so 4 CTAs fit per SM
-// (measured: 1.12 vs 1.18 ms per GiB, cfg2), at the cost of one more barrier
-// per tile.
-#ifndef VT_NSTAGE
-#define VT_NSTAGE 1
-#endif
-constexpr int kNStage = VT_NSTAGE;
-
+// Staging buffers per CTA (Codec::kNStage):
+//   1: tile j-1 is copied out before tile j is decoded into the same buffer
+//      (copy, barrier, emit);
+//   2: tile j is decoded first and tile j-1 is copied out afterwards, which
+//      gives tile j-1's look-back one more decode phase of slack before the
+//      compute warps wait for its offset.
+// Two buffers fit 4 CTAs per SM only for the UTF-16 -> UTF-8 tile (24 KiB of
+// staging); the UTF-8 -> UTF-16 tile needs 32 KiB and uses one (measured: 4
+// CTAs with one buffer beat 3 CTAs with two, 1.12 vs 1.18 ms per GiB).
 template <class C>
 struct PipeSmem {
   alignas(16) uint8_t pad0[32];
-  alignas(16) uint8_t out[kNStage][C::kStageBytes + 32];
+  alignas(16) uint8_t out[C::kNStage][C::kStageBytes + 32];
   alignas(16) uint8_t pad1[32];
   unsigned scan[kComputeThreads / 32];
   unsigned red[kComputeThreads / 32];
   unsigned tile;
-  // hand-off between the compute warps and the look-back warp (2-slot rings
-  // indexed by tile parity, guarded by the named barriers below)
-  unsigned lb_tile[2], agg[2];
+  // hand-off between the compute warps and the look-back warp (rings indexed
+  // by the CTA-local tile number, guarded by the named barriers below)
+  unsigned lb_tile[4], agg[2];
   unsigned long long excl[2];
 };
 
@@ -108,30 +109,56 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
            kComputeThreads);
 }
 
-// Hand-off barriers (all kPipeBlock threads), two ids per kind indexed by the
-// CTA-local tile number j & 1:
-//   BAR_GRAB: compute warps arrive once tile j's id is in shared memory; the
-//             look-back warp waits, then resolves tile j's exclusive prefix
-//             while the compute warps count and decode it;
-//   BAR_AGG:  compute warps arrive once tile j's aggregate is in shared memory;
-//             the look-back warp waits, publishes tile j's inclusive prefix;
-//   BAR_EXCL: the look-back warp arrives once tile j's offset is in shared
-//             memory; the compute warps wait before copying tile j out (during
-//             tile j+1).
+// Hand-off barriers (all kPipeBlock threads), indexed by the CTA-local tile
+// number j:
+//   BAR_GRAB + (j & 3): compute warps arrive once tile j's id is in shared
+//             memory; the look-back warp waits, then resolves tile j's
+//             exclusive prefix while the compute warps count and decode it;
+//   BAR_AGG + (j & 1):  compute warps arrive once tile j's aggregate is in
+//             shared memory; the look-back warp waits, publishes tile j's
+//             inclusive prefix;
+//   BAR_EXCL + (j & 1): the look-back warp arrives once tile j's offset is in
+//             shared memory; the compute warps wait before copying tile j out
+//             (during tile j+1).
 // bar.arrive orders the producer's prior shared-memory writes before the
 // consumer's bar.sync returns, and a waiting warp issues nothing (no polling).
-// At most one instance per id is pending: every arrival for tile j+2 happens
-// after the compute warps waited for tile j's offset, which the look-back warp
-// only publishes after its waits for tile j completed.
-constexpr int BAR_GRAB = 2, BAR_EXCL = 4, BAR_AGG = 6;
+// At most one instance per id is pending:
+//   AGG(j+2) is arrived at after the compute warps waited for EXCL(j), which
+//     the look-back warp arrives at only after its wait on AGG(j);
+//   EXCL(j+2) is arrived at after the look-back warp's wait on AGG(j+2), which
+//     follows the compute warps' wait on EXCL(j);
+//   GRAB(j+4) is arrived at after the compute warps waited for EXCL(j+2) (one
+//     buffer) or EXCL(j+1) (two buffers), which the look-back warp arrives at
+//     only after its wait on GRAB(j+2) or GRAB(j+1), so after GRAB(j) -- two
+//     ids per kind are not enough for GRAB with two buffers, where GRAB(j+2)
+//     is arrived at while the look-back warp may still be before GRAB(j+1).
+constexpr int BAR_EXCL = 2, BAR_AGG = 4, BAR_GRAB = 8;
+
+#ifdef VT_PHASES
+// per-phase cycle totals of warp 0 of every CTA (perf probe): loop-top sync,
+// count, EXCL wait, copy-out, post-copy sync, emit, grab; [7] = tiles
+__device__ unsigned long long g_phase[8];
+#define VT_PH(i)                                                  \
+  do {                                                            \
+    const long long _t = clock64();                               \
+    if (threadIdx.x == 0) atomicAdd(&g_phase[i], (unsigned long long)(_t - ph_t)); \
+    ph_t = _t;                                                    \
+  } while (0)
+#else
+#define VT_PH(i) \
+  do {           \
+  } while (0)
+#endif
 
 template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
+  constexpr int NS = C::kNStage;
+  static_assert(NS == 1 || NS == 2, "one or two staging buffers");
   if (threadIdx.x >= kComputeThreads) {
     const bool leader = threadIdx.x == kComputeThreads;
     for (unsigned j = 0;; j++) {
-      bar_sync(BAR_GRAB + (j & 1), kPipeBlock);
-      const unsigned tile = sm.lb_tile[j & 1];
+      bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
+      const unsigned tile = sm.lb_tile[j & 3];
       if (tile >= a.ntiles) break;
       unsigned long long excl = 0;
       if (tile != 0) {
@@ -162,10 +189,33 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
     }
     bar_arrive(BAR_GRAB, kPipeBlock);
     unsigned j = 0, prev_agg = 0;
+#ifdef VT_PHASES
+    long long ph_t = clock64();
+#endif
+    // tile j-1's offset was resolved meanwhile: copy it out
+    auto copy_prev = [&]() {
+#ifdef VT_PROBE
+      const long long t0 = clock64();
+#endif
+      bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
+      VT_PH(2);
+#ifdef VT_PROBE
+      if (threadIdx.x == 0) {
+        atomicAdd(&a.ctl->pad[2], (unsigned long long)(clock64() - t0));
+        atomicAdd(&a.ctl->pad[3], 1ull);
+      }
+#endif
+      copy_tile_out<C>(a, sm.out[(j - 1) % NS], sm.excl[(j - 1) & 1], prev_agg);
+      VT_PH(3);
+    };
     while (true) {
       ComputeSync::sync();
+      VT_PH(0);
       const unsigned tile = sm.tile;
       if (tile >= a.ntiles) break;
+      // a stale error only means a dead tile is processed (its output is
+      // dropped at copy-out, its look-back gives up)
+      const unsigned long long err_seen = threadIdx.x == 0 ? load_relaxed(&a.ctl->err) : 0ull;
       typename C::TileCount tc;
       unsigned off, agg;
       C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
@@ -176,37 +226,37 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         sm.agg[j & 1] = agg;
       }
       bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
-      if (j > 0) {
-        // tile j-1: its offset was resolved meanwhile; copy it out
-#ifdef VT_PROBE
-        const long long t0 = clock64();
-#endif
-        bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
-#ifdef VT_PROBE
-        if (threadIdx.x == 0) {
-          atomicAdd(&a.ctl->pad[2], (unsigned long long)(clock64() - t0));
-          atomicAdd(&a.ctl->pad[3], 1ull);
-        }
-#endif
-        copy_tile_out<C>(a, sm.out[(j - 1) % kNStage], sm.excl[(j - 1) & 1], prev_agg);
-        if (kNStage == 1) ComputeSync::sync();
+      VT_PH(1);
+      if (NS == 1 && j > 0) {
+        copy_prev();
+        ComputeSync::sync();  // the buffer is free
+        VT_PH(4);
       }
 #ifndef VT_EXP_NOEMIT
-      C::emit(a, tc, sm.out[j % kNStage], off);
+      C::emit(a, tc, sm.out[j % NS], off);
 #endif
+      VT_PH(5);
       if (threadIdx.x == 0) {
-        const unsigned t = grab_tile(a, C::kTileElems);
+        // (the error word was read at the top of the tile: one round trip
+        // less on the path every warp waits for at the loop-top barrier)
+        unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
+        if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
+          t = a.ntiles;
         sm.tile = t;
-        sm.lb_tile[(j + 1) & 1] = t;
+        sm.lb_tile[(j + 1) & 3] = t;
       }
-      bar_arrive(BAR_GRAB + ((j + 1) & 1), kPipeBlock);
+      bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
+      VT_PH(6);
+#ifdef VT_PHASES
+      if (threadIdx.x == 0) atomicAdd(&g_phase[7], 1ull);
+#endif
+      // two buffers: tile j-1 goes out after tile j was decoded (the loop-top
+      // barrier orders this copy before tile j+1 is decoded into its buffer)
+      if (NS == 2 && j > 0) copy_prev();
       prev_agg = agg;
       j++;
     }
-    if (j > 0) {
-      bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
-      copy_tile_out<C>(a, sm.out[(j - 1) % kNStage], sm.excl[(j - 1) & 1], prev_agg);
-    }
+    if (j > 0) copy_prev();
   }
   finalize_if_last(a, true, C::kTileElems);
 }
