@@ -207,19 +207,7 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   const bool interior =
       vt0 - 2 >= (long long)a.head && vt0 + K16_TILE + 2 <= (long long)(a.head + a.n);
   if (interior) {
-    const uint4* p = reinterpret_cast<const uint4*>(a.base + tc.v0);
-#pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const uint4 v = __ldg(p + r);
-      tc.W.w[1 + 4 * r] = v.x; tc.W.w[2 + 4 * r] = v.y;
-      tc.W.w[3 + 4 * r] = v.z; tc.W.w[4 + 4 * r] = v.w;
-    }
-    uint32_t pw = __shfl_up_sync(0xffffffffu, tc.W.w[K16_WPT], 1);
-    uint32_t nw = __shfl_down_sync(0xffffffffu, tc.W.w[1], 1);
-    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 - 2));
-    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 + K16_UPT));
-    tc.W.w[0] = pw;
-    tc.W.w[K16_WPT + 1] = nw;
+    load_lane_words<K16_WPT>(reinterpret_cast<const uint8_t*>(a.base + tc.v0), lane, tc.W.w);
     if (kBE) {
 #pragma unroll
       for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = prmt(tc.W.w[k], 0, 0x2301);
@@ -445,19 +433,7 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
     const bool interior = r0 - 2 >= head && r0 + K16_ROW + 2 <= end;
     Words16 W;
     if (interior) {
-      const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const uint4 v = __ldg(p + r);
-        W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y;
-        W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
-      }
-      uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K16_WPT], 1);
-      uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
-      if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 2));
-      if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K16_UPT));
-      W.w[0] = pw;
-      W.w[K16_WPT + 1] = nw;
+      load_lane_words<K16_WPT>(reinterpret_cast<const uint8_t*>(a.base + v0), lane, W.w);
       if (kBE) {
 #pragma unroll
         for (int k = 0; k < K16_WPT + 2; k++) W.w[k] = prmt(W.w[k], 0, 0x2301);
@@ -586,7 +562,9 @@ int occupancy_utf16(bool transcode) {
 
 #ifdef VT_PHASES
 int read_phases16(unsigned long long* out8) {
-  return (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+  int rc = (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+  if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 8, g_phase_sub, sizeof(g_phase_sub));
+  return rc;
 }
 #endif
 

@@ -38,6 +38,9 @@ constexpr int K8_WPT = VT_K8_WPT;               // words per thread
 constexpr int K8_BPT = 4 * K8_WPT;              // bytes per thread
 constexpr int K8_TILE = K8_THREADS * K8_BPT;    // bytes per tile
 constexpr unsigned kNone = 0xFFFFFFFFu;
+#ifndef VT_FOUR_EMIT
+#define VT_FOUR_EMIT 2  // 1: separate low-surrogate stores (8 per word)
+#endif
 constexpr uint32_t H = 0x80808080u;
 
 __device__ __forceinline__ unsigned leadlen(unsigned b) {
@@ -296,6 +299,65 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   }
 }
 
+// Words with 4-byte characters: one unit per lane, like the BMP form.  A
+// 4-byte lead's lane writes the high surrogate, and the first continuation
+// after it (an "ls lane") writes the low surrogate: 0xDC00 | (cp & 0x3FF) is
+// made of the two bytes after that lane exactly like a 3-byte character's
+// unit is made of the two bytes after its lead (lo plane), with DC | (b >> 2)
+// & 3 as the high byte.  So every lane stores at most one unit (4 predicated
+// stores per word, not 8).  `carry4` (bit 7) says the previous word's lane 3
+// was a 4-byte lead of this thread; a lead in the thread's last byte has its
+// ls lane in the next thread and is finished by emit_tail_ls.
+template <bool kBE>
+__device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t& q,
+                                               uint32_t& carry4) {
+  const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
+  const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
+  const uint32_t c2 = c << 1;
+  const uint32_t lead7 = ~(c & ~c2) & H;
+  const uint32_t ge_e0 = c & c2 & (c << 2);            // bit 7: 3-byte or 4-byte lead
+  const uint32_t four7 = ge_e0 & (c << 3) & H;         // 4-byte lead
+  const uint32_t ls7 = (four7 << 8) | carry4;          // first continuation after one
+  carry4 = four7 >> 24;
+  const uint32_t mna = prmt(c, 0, 0xBA98);
+  const uint32_t m3 = prmt(ge_e0 | ls7, 0, 0xBA98);    // unit from the two bytes after
+  const uint32_t mls = prmt(ls7, 0, 0xBA98);
+  const uint32_t A = (n1 & m3) | (c & ~m3);
+  const uint32_t B = (n2 & m3) | (n1 & ~m3);
+  const uint32_t lom = ((A << 6) & 0xC0C0C0C0u) | (B & 0x3F3F3F3Fu);
+  const uint32_t lo = (c & ~mna) | (lom & mna);
+  const uint32_t him = (((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3)) & mna;
+  const uint32_t hi_ls = ((n1 >> 2) & 0x03030303u) | 0xDCDCDCDCu;
+  const uint32_t hi = lop3<0xCA>(mls, hi_ls, him);
+  uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140), u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
+  // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10)
+  const uint32_t m4 = prmt(four7, 0, 0xBA98);
+  const uint32_t X = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
+  const uint32_t c7 = c & 0x07070707u;
+  uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
+  uint32_t hs23 = prmt(X, c7, 0x7362) + 0xD7C0D7C0u;
+  if (kBE) {
+    hs01 = prmt(hs01, 0, 0x2301);
+    hs23 = prmt(hs23, 0, 0x2301);
+  }
+  u01 = lop3<0xCA>(prmt(m4, 0, 0x1100), hs01, u01);
+  u23 = lop3<0xCA>(prmt(m4, 0, 0x3322), hs23, u23);
+  const uint32_t st7 = lead7 | ls7;
+  if (st7 & 0x00000080u) { sts16(q, u01); q += 2; }
+  if (st7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
+  if (st7 & 0x00800000u) { sts16(q, u23); q += 2; }
+  if (st7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
+}
+
+// The low surrogate of a 4-byte character whose lead is the thread's last
+// byte: its ls lane is byte 0 of the next word n (bytes 1 and 2 of n follow).
+template <bool kBE>
+__device__ __forceinline__ void emit_tail_ls(uint32_t n, uint32_t q) {
+  const uint32_t b2 = (n >> 8) & 0xFFu, b3 = (n >> 16) & 0xFFu;
+  const uint32_t u = 0xDC00u | ((b2 & 0x0Fu) << 6) | (b3 & 0x3Fu);
+  sts16(q, kBE ? (((u & 0xFFu) << 8) | (u >> 8)) : u);
+}
+
 // ---- per-tile front half: load, classify, locate errors, count -------------
 struct TileCount {
   Words W;
@@ -318,29 +380,33 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   const bool interior =
       vt0 - 4 >= (long long)a.head && vt0 + K8_TILE + 4 <= (long long)(a.head + a.n);
   if (interior) {
-    const uint4* p = reinterpret_cast<const uint4*>(a.base + tc.v0);
-#pragma unroll
-    for (int r = 0; r < K8_WPT / 4; r++) {
-      const uint4 v = __ldg(p + r);
-      tc.W.w[1 + 4 * r] = v.x; tc.W.w[2 + 4 * r] = v.y;
-      tc.W.w[3 + 4 * r] = v.z; tc.W.w[4 + 4 * r] = v.w;
-    }
-    uint32_t pw = __shfl_up_sync(0xffffffffu, tc.W.w[K8_WPT], 1);
-    uint32_t nw = __shfl_down_sync(0xffffffffu, tc.W.w[1], 1);
-    if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 - 4));
-    if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + tc.v0 + K8_BPT));
-    tc.W.w[0] = pw;
-    tc.W.w[K8_WPT + 1] = nw;
+    load_lane_words<K8_WPT>(a.base + tc.v0, lane, tc.W.w);
   } else {
     Words L;
     load_masked(src, tc.v0, L);
 #pragma unroll
     for (int k = 0; k < K8_WPT + 2; k++) tc.W.w[k] = L.w[k];
   }
+#ifdef VT_PHASES
+  {  // sub-phase probe: wait for the loads
+    uint32_t z = 0;
+#pragma unroll
+    for (int k = 0; k < K8_WPT + 2; k++) z ^= tc.W.w[k];
+    if (z == 0x9E3779B9u) asm volatile("trap;");
+    const long long t = clock64();
+    if (threadIdx.x == 0) atomicAdd(&g_phase_sub[0], (unsigned long long)t);
+  }
+#endif
   const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
   tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
   const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
   const ClassOut co = classify(tc.W, a.k);
+#ifdef VT_PHASES
+  {
+    const long long t = clock64() + (co.units == 0x7FFFFFFF ? 1 : 0);
+    if (threadIdx.x == 0) atomicAdd(&g_phase_sub[1], (unsigned long long)t);
+  }
+#endif
   tc.four = co.four;
   tc.lim = hi;
   unsigned my_err = kNone;
@@ -389,8 +455,15 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
 #pragma unroll
       for (int k = 1; k <= K8_WPT; k++) emit_word<false, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
+#if VT_FOUR_EMIT == 2
+      uint32_t carry4 = 0;  // a lead in the previous thread finishes its own pair
+#pragma unroll
+      for (int k = 1; k <= K8_WPT; k++) emit_word_four<kBE>(tc.W.w[k], tc.W.w[k + 1], q, carry4);
+      if (carry4) emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
+#else
 #pragma unroll
       for (int k = 1; k <= K8_WPT; k++) emit_word<true, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
+#endif
     }
   } else {
     generic_chars(Src{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off, kBE);
@@ -468,19 +541,7 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
     const bool interior = r0 - 4 >= head && r0 + K8_ROW + 4 <= end;
     Words W;
     if (interior) {
-      const uint4* p = reinterpret_cast<const uint4*>(a.base + v0);
-#pragma unroll
-      for (int r = 0; r < K8_WPT / 4; r++) {
-        const uint4 v = __ldg(p + r);
-        W.w[1 + 4 * r] = v.x; W.w[2 + 4 * r] = v.y;
-        W.w[3 + 4 * r] = v.z; W.w[4 + 4 * r] = v.w;
-      }
-      uint32_t pw = __shfl_up_sync(0xffffffffu, W.w[K8_WPT], 1);
-      uint32_t nw = __shfl_down_sync(0xffffffffu, W.w[1], 1);
-      if (lane == 0) pw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 - 4));
-      if (lane == 31) nw = __ldg(reinterpret_cast<const uint32_t*>(a.base + v0 + K8_BPT));
-      W.w[0] = pw;
-      W.w[K8_WPT + 1] = nw;
+      load_lane_words<K8_WPT>(a.base + v0, lane, W.w);
     } else {
       load_masked(src, v0, W);
     }
@@ -604,7 +665,9 @@ int occupancy_utf8(bool transcode) {
 
 #ifdef VT_PHASES
 int read_phases(unsigned long long* out8) {
-  return (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+  int rc = (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
+  if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 8, g_phase_sub, sizeof(g_phase_sub));
+  return rc;
 }
 #endif
 

@@ -269,6 +269,32 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   }
 }
 
+// A lane's 4*NW input bytes at p (16-byte aligned) as NW words w[1..NW], plus
+// the word before (w[0]) and after (w[NW+1]) its range: neighbour lanes' words
+// by shuffle, lanes 0 and 31 load theirs.  Every lane issues one halo load
+// (address selected, no branch), so all loads are in flight together -- a halo
+// load behind the shuffles, which wait for the body, would add a second load
+// latency to the tile.  p - 4 and p + 4*NW must be readable for lanes 0 / 31.
+template <int NW>
+__device__ __forceinline__ void load_lane_words(const uint8_t* p, unsigned lane, uint32_t* w) {
+  static_assert(NW % 4 == 0, "whole 16-byte loads");
+  const uint32_t* hp = reinterpret_cast<const uint32_t*>(lane == 0 ? p - 4 : p + 4 * NW);
+  const uint32_t h = __ldg(hp);
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int r = 0; r < NW / 4; r++) {
+    const uint4 v = __ldg(q + r);
+    w[1 + 4 * r] = v.x;
+    w[2 + 4 * r] = v.y;
+    w[3 + 4 * r] = v.z;
+    w[4 + 4 * r] = v.w;
+  }
+  const uint32_t pw = __shfl_up_sync(0xffffffffu, w[NW], 1);
+  const uint32_t nw = __shfl_down_sync(0xffffffffu, w[1], 1);
+  w[0] = lane == 0 ? h : pw;
+  w[NW + 1] = lane == 31 ? h : nw;
+}
+
 // proj/src/codec_core.cpp:5-38 on a 4-byte window (bytes past the input are
 // zero, which fails exactly like the truncation test at :28).
 __device__ __forceinline__ bool decode_ok(uint32_t v) {

@@ -138,6 +138,9 @@ constexpr int BAR_EXCL = 2, BAR_AGG = 4, BAR_GRAB = 8;
 // per-phase cycle totals of warp 0 of every CTA (perf probe): loop-top sync,
 // count, EXCL wait, copy-out, post-copy sync, emit, grab; [7] = tiles
 __device__ unsigned long long g_phase[8];
+// count sub-phases (thread 0, absolute clocks summed): [0] loads arrived,
+// [1] classify done; read against the count phase's start/end
+__device__ unsigned long long g_phase_sub[4];
 #define VT_PH(i)                                                  \
   do {                                                            \
     const long long _t = clock64();                               \
@@ -211,6 +214,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
     while (true) {
       ComputeSync::sync();
       VT_PH(0);
+#ifdef VT_PHASES
+      if (threadIdx.x == 0) atomicAdd(&g_phase_sub[2], (unsigned long long)ph_t);
+#endif
       const unsigned tile = sm.tile;
       if (tile >= a.ntiles) break;
       // a stale error only means a dead tile is processed (its output is
@@ -227,6 +233,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       }
       bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
       VT_PH(1);
+#ifdef VT_PHASES
+      if (threadIdx.x == 0) atomicAdd(&g_phase_sub[3], (unsigned long long)ph_t);
+#endif
       if (NS == 1 && j > 0) {
         copy_prev();
         ComputeSync::sync();  // the buffer is free
@@ -240,6 +249,17 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         // (the error word was read at the top of the tile: one round trip
         // less on the path every warp waits for at the loop-top barrier)
         unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
+#ifdef VT_PREFETCH
+        {  // experiment: ask L2 for the input of the tile taken ~one round later
+          constexpr unsigned kEB = sizeof(*a.base);
+          const unsigned long long pt = (unsigned long long)t + VT_PREFETCH * gridDim.x;
+          if (pt + 1 < a.ntiles)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             reinterpret_cast<const char*>(a.base) + pt * C::kTileElems * kEB),
+                         "r"(C::kTileElems * kEB)
+                         : "memory");
+        }
+#endif
         if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
           t = a.ntiles;
         sm.tile = t;

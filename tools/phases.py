@@ -16,12 +16,16 @@ for cfg in [int(c) for c in (sys.argv[1:] or ["2", "3"])]:
         run = lambda: vt.utf8_to_utf16_device(d, n, o, d_res=res)
     for _ in range(3): run()
     torch.cuda.synchronize()
-    b0 = np.zeros(8, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b0.ctypes.data)
+    b0 = np.zeros(12, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b0.ctypes.data)
     for _ in range(5): run()
     torch.cuda.synchronize()
-    b = np.zeros(8, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b.ctypes.data)
+    b = np.zeros(12, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b.ctypes.data)
     b = (b - b0).astype(np.float64); t = b[7]
     tot = b[:7].sum() / t
+    sub = ""
+    if b[8] > 0:
+        sub = f"  [count: loads {b[1] / t - (b[9] - b[8]) / t - (b[11] - b[9]) / t:.0f}, classify {(b[9] - b[8]) / t:.0f}, scan+publish {(b[11] - b[9]) / t:.0f}]"
+    print(sub)
     print(f"cfg{cfg}: cycles per tile (warp 0) total {tot:.0f}: " +
           ", ".join(f"{nm} {b[i] / t:.0f}" for i, nm in enumerate(names)))
     del d, o
