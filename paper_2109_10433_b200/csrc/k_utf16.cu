@@ -81,6 +81,44 @@ __device__ __noinline__ void load_masked16(Src16 a, long long v0, Words16& W) {
   }
 }
 
+// One word straddling an end of the input, unit by unit (rare; out of line).
+__device__ __noinline__ uint32_t straddle_word16(Src16 a, long long p) {
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  uint32_t x = 0;
+  for (int b = 0; b < 2; b++) {
+    if (p + b >= lo && p + b < hi) {
+      uint32_t u = a.base[p + b];
+      if (a.be) u = ((u & 0xFFu) << 8) | (u >> 8);
+      x |= u << (16 * b);
+    }
+  }
+  return x;
+}
+
+// A thread's window at the ends of the input, units outside [head, head + n)
+// as 0x0000 (as load_edge in k_utf8.cu): whole words at once, the at most two
+// straddling words unit by unit.  Zeros are ASCII, so an end tile takes the
+// SWAR path (counts minus the zeros); a surrogate cut from its partner by an
+// end still shows as a pairing error.
+template <bool kBE>
+__device__ __forceinline__ void load_edge16(Src16 a, long long v0, uint32_t* w) {
+  constexpr int NW = K16_WPT + 2;
+  const long long s0 = v0 - 2;  // virtual unit position of word 0
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  const int kf = (int)max(0LL, min((long long)NW, (lo - s0 + 1) >> 1));  // words [kf, kl)
+  const int kl = (int)max((long long)kf, min((long long)NW, (hi - s0) >> 1));  // are inside
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(a.base + s0);
+#pragma unroll
+  for (int k = 0; k < NW; k++) {
+    const uint32_t x = (k >= kf && k < kl) ? __ldg(wp + k) : 0u;
+    w[k] = kBE ? prmt(x, 0, 0x2301) : x;
+  }
+#pragma unroll
+  for (int k = 0; k < NW; k++)
+    if ((k == kf - 1 || k == kl) && s0 + 2 * k + 2 > lo && s0 + 2 * k < hi)
+      w[k] = straddle_word16(a, s0 + 2 * k);
+}
+
 __device__ __forceinline__ bool is_hi(unsigned u) { return (u & 0xFC00u) == 0xD800u; }
 __device__ __forceinline__ bool is_lo(unsigned u) { return (u & 0xFC00u) == 0xDC00u; }
 
@@ -213,10 +251,7 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
       for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = prmt(tc.W.w[k], 0, 0x2301);
     }
   } else {
-    Words16 L;
-    load_masked16(src, tc.v0, L);
-#pragma unroll
-    for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = L.w[k];
+    load_edge16<kBE>(src, tc.v0, tc.W.w);
   }
   const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
   tc.lo = (unsigned)max(0LL, min((long long)K16_UPT, s));
@@ -224,14 +259,15 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   tc.lim = hi;
   const Class16 c = classify16(tc.W);
   unsigned my_err = kNone16;
-  if (c.err || !interior) {
+  if (c.err) {
     const unsigned er = first_error16(src, tc.v0, tc.lo, hi);
     if (er != kNone16) my_err = K16_UPT * threadIdx.x + er;
   }
-  if (interior) {
+  {
     constexpr int kErrShift = NT <= 256 ? 23 : 22;  // NT << kErrShift <= 2^31
     static_assert(NT <= 512 && 4 * K16_TILE < (1 << kErrShift), "packed scan fields");
-    tc.cnt = kTranscode ? c.bytes : c.chars;
+    // (end tiles: the zeros outside the input counted as one ASCII unit each)
+    tc.cnt = (kTranscode ? c.bytes : c.chars) - (K16_UPT - (hi - tc.lo));
     unsigned total;
     off = block_excl_scan<NT, Sync, false>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), scan, total);
     if ((total >> kErrShift) == 0) {
@@ -390,7 +426,9 @@ struct Utf16Codec {
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
                                               unsigned off) {
     if (tc.simple) {
-      uint32_t q = smem_addr(stage) + off;
+      // (tc.lo > 0 only for the first thread of a call: the zeros before the
+      // input are encoded too and land in the pad before the staging buffer)
+      uint32_t q = smem_addr(stage) + off - tc.lo;
 #if VT_U16_EMIT == 3
 #pragma unroll
       for (int k = 1; k < K16_WPT; k++) emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q);
@@ -439,12 +477,14 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
         for (int k = 0; k < K16_WPT + 2; k++) W.w[k] = prmt(W.w[k], 0, 0x2301);
       }
     } else {
-      load_masked16(src, v0, W);
+      load_edge16<kBE>(src, v0, W.w);
     }
     const Class16 c = classify16(W);
     unsigned cnt;
-    if (interior && !c.err) {
-      cnt = kUnits ? c.bytes : c.chars;
+    if (!c.err) {
+      const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
+      const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
+      cnt = (kUnits ? c.bytes : c.chars) - (K16_UPT - (hi - lo));  // minus the zeros outside
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));

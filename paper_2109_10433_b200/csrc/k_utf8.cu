@@ -77,6 +77,36 @@ __device__ __noinline__ void load_masked(Src a, long long v0, Words& W) {
   }
 }
 
+// One word straddling an end of the input, byte by byte (rare; out of line).
+__device__ __noinline__ uint32_t straddle_word(Src a, long long p) {
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  uint32_t x = 0;
+  for (int b = 0; b < 4; b++)
+    if (p + b >= lo && p + b < hi) x |= (uint32_t)a.base[p + b] << (8 * b);
+  return x;
+}
+
+// A thread's window at the ends of the input, bytes outside [head, head + n)
+// as 0x00: the whole words inside the input are loaded at once (they are
+// 4-byte aligned in the virtual range), the at most two straddling words byte
+// by byte.  Zeros are ASCII to the classification, so an end tile takes the
+// SWAR path like any other (its counts minus the zeros); a character cut by an
+// end, or a continuation byte at the start, still shows as a structure error.
+__device__ __forceinline__ void load_edge(Src a, long long v0, uint32_t* w) {
+  constexpr int NW = K8_WPT + 2;
+  const long long s0 = v0 - 4;  // virtual position of word 0
+  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
+  const int kf = (int)max(0LL, min((long long)NW, (lo - s0 + 3) >> 2));  // words [kf, kl)
+  const int kl = (int)max((long long)kf, min((long long)NW, (hi - s0) >> 2));  // are inside
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(a.base + s0);
+#pragma unroll
+  for (int k = 0; k < NW; k++) w[k] = (k >= kf && k < kl) ? __ldg(wp + k) : 0u;
+#pragma unroll
+  for (int k = 0; k < NW; k++)
+    if ((k == kf - 1 || k == kl) && s0 + 4 * k + 4 > lo && s0 + 4 * k < hi)
+      w[k] = straddle_word(a, s0 + 4 * k);
+}
+
 // Exact first error among positions [lo, hi) of the thread's bytes.  Rare
 // path: reloads the thread's window itself (byte loads), so the hot path keeps
 // its words in registers.
@@ -382,10 +412,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   if (interior) {
     load_lane_words<K8_WPT>(a.base + tc.v0, lane, tc.W.w);
   } else {
-    Words L;
-    load_masked(src, tc.v0, L);
-#pragma unroll
-    for (int k = 0; k < K8_WPT + 2; k++) tc.W.w[k] = L.w[k];
+    load_edge(src, tc.v0, tc.W.w);
   }
 #ifdef VT_PHASES
   {  // sub-phase probe: wait for the loads
@@ -410,16 +437,17 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   tc.four = co.four;
   tc.lim = hi;
   unsigned my_err = kNone;
-  if (co.viol || !interior) {
+  if (co.viol) {
     const unsigned er = first_error_rule_a(src, tc.v0, tc.lo, hi);
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
-  if (interior) {
+  {
     // fast path: one scan; bits kErrShift..31 count the threads that found an error
     // (NT << kErrShift <= 2^31: no wrap; counts stay below 2^kErrShift)
     constexpr int kErrShift = NT <= 256 ? 23 : 22;  // NT << kErrShift <= 2^31
     static_assert(NT <= 512 && 2 * K8_TILE < (1 << kErrShift), "packed scan fields");
-    tc.cnt = kTranscode ? co.units : co.chars;
+    // (end tiles: the zeros outside the input counted as one ASCII character each)
+    tc.cnt = (kTranscode ? co.units : co.chars) - (K8_BPT - (hi - tc.lo));
     unsigned total;
     off = block_excl_scan<NT, Sync, false>(my_err == kNone ? tc.cnt : (1u << kErrShift), scan, total);
     if ((total >> kErrShift) == 0) {
@@ -448,7 +476,9 @@ template <bool kBE>
 __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
                                           unsigned off) {
   if (tc.simple) {
-    uint32_t q = smem_addr(stage) + 2u * off;
+    // (tc.lo > 0 only for the first thread of a call: the zeros before the
+    // input are decoded too and land in the pad before the staging buffer)
+    uint32_t q = smem_addr(stage) + 2u * off - 2u * tc.lo;
     // warp-uniform choice (the 4-byte-capable form handles every word): a
     // per-thread choice would run both forms in mixed warps
     if (!__any_sync(0xffffffffu, tc.four)) {
@@ -543,12 +573,14 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
     if (interior) {
       load_lane_words<K8_WPT>(a.base + v0, lane, W.w);
     } else {
-      load_masked(src, v0, W);
+      load_edge(src, v0, W.w);
     }
     const ClassOut co = classify(W, a.k);
     unsigned cnt;
-    if (interior && !co.viol) {
-      cnt = kUnits ? co.units : co.chars;
+    if (!co.viol) {
+      const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
+      const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
+      cnt = (kUnits ? co.units : co.chars) - (K8_BPT - (hi - lo));  // minus the zeros outside
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));

@@ -6,8 +6,11 @@ import paper_2109_10433_b200 as vt
 L = vt.lib(); L.vt_debug_phases.argtypes = [C.c_int, C.c_void_p]
 names = ["top-sync", "count", "excl-wait", "copy-out", "post-copy-sync", "emit", "grab"]
 res = torch.zeros(3, dtype=torch.int64, device="cuda")
-for cfg in [int(c) for c in (sys.argv[1:] or ["2", "3"])]:
-    d, n, _ = vt.generate(cfg, 1 << 29 if cfg == 3 else 1 << 30)
+for spec in (sys.argv[1:] or ["2", "3"]):
+    cfg, _, sz = spec.partition(":")  # "1:16" = cfg1 at 16 MiB
+    cfg = int(cfg)
+    size = (int(sz) << 20) if sz else (1 << 30)
+    d, n, _ = vt.generate(cfg, size // 2 if cfg == 3 else size)
     if cfg == 3:
         o = torch.empty(3 * n + 16, dtype=torch.uint8, device="cuda")
         run = lambda: vt.utf16_to_utf8_device(d, n, o, d_res=res)
