@@ -60,27 +60,6 @@ struct Words16 {
   uint32_t w[K16_WPT + 2];  // w[0] = previous word, w[1..16] own, w[17] next
 };
 
-__device__ __forceinline__ unsigned unit_at(const Words16& W, int i) {  // i in [-2, 34)
-  const int q = i + 2;
-  return (W.w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu;
-}
-
-__device__ __noinline__ void load_masked16(Src16 a, long long v0, Words16& W) {
-  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
-  for (int k = 0; k < K16_WPT + 2; k++) {
-    uint32_t x = 0;
-    for (int b = 0; b < 2; b++) {
-      const long long p = v0 - 2 + 2 * k + b;
-      if (p >= lo && p < hi) {
-        uint32_t u = a.base[p];
-        if (a.be) u = ((u & 0xFFu) << 8) | (u >> 8);
-        x |= u << (16 * b);
-      }
-    }
-    W.w[k] = x;
-  }
-}
-
 // One word straddling an end of the input, unit by unit (rare; out of line).
 __device__ __noinline__ uint32_t straddle_word16(Src16 a, long long p) {
   const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
@@ -148,35 +127,54 @@ __device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned pv, unsigne
   return 0x8080E0u | (u >> 12) | (((u >> 6) & 0x3Fu) << 8) | ((u & 0x3Fu) << 16);
 }
 
-// Masked per-unit path (ends of the input, tiles with an error): exact first
-// error among [lo, hi), or with `count`: bytes / code points of [lo, lim).
-__device__ __noinline__ unsigned first_error16(Src16 a, long long v0, unsigned lo, unsigned hi) {
-  Words16 W;
-  load_masked16(a, v0, W);
-  for (unsigned i = lo; i < hi; i++) {
-    const unsigned u = unit_at(W, (int)i);
-    if (is_lo(u) && !is_hi(unit_at(W, (int)i - 1))) return i;
-    if (is_hi(u) && !is_lo(unit_at(W, (int)i + 1))) return i;
+// Exact path (tiles with an error) on a copy of the caller's window, one loop
+// step per word (both units) with the neighbouring words in registers, so
+// the hot path keeps its words in registers and nothing is reloaded.
+// first_error16: the smallest unit in [lo, hi) failing the pairing rule C of
+// SURVEY.md 8(a) (a low surrogate not after a high one, a high one not before
+// a low one); generic_units: bytes (or code points) of units [lo, lim), with
+// `dst` also their UTF-8 bytes.
+__device__ __noinline__ unsigned first_error16(const Words16& W, unsigned lo, unsigned hi) {
+  uint32_t pw = W.w[0], cw = W.w[1];
+  for (int k = 0; k < K16_WPT; k++) {
+    const uint32_t nw = W.w[k + 2];
+    const unsigned u0 = cw & 0xFFFFu, u1 = cw >> 16;
+    const unsigned i = 2 * k;
+    if (i >= lo && i < hi &&
+        ((is_lo(u0) && !is_hi(pw >> 16)) || (is_hi(u0) && !is_lo(u1))))
+      return i;
+    if (i + 1 >= lo && i + 1 < hi &&
+        ((is_lo(u1) && !is_hi(u0)) || (is_hi(u1) && !is_lo(nw & 0xFFFFu))))
+      return i + 1;
+    pw = cw;
+    cw = nw;
   }
   return kNone16;
 }
 
-__device__ __noinline__ unsigned generic_units(Src16 a, long long v0, unsigned lo, unsigned lim,
+__device__ __noinline__ unsigned generic_units(const Words16& W, unsigned lo, unsigned lim,
                                                bool bytes, uint8_t* dst) {
-  Words16 W;
-  load_masked16(a, v0, W);
   unsigned q = 0;
-  for (unsigned i = lo; i < lim; i++) {
-    const unsigned u = unit_at(W, (int)i);
-    unsigned len;
-    const uint32_t p = encode_unit(u, unit_at(W, (int)i - 1), len);
-    if (!bytes) {
-      q += is_lo(u) ? 0u : 1u;
-      continue;
+  uint32_t pw = W.w[0];
+  for (int k = 0; k < K16_WPT; k++) {
+    const uint32_t cw = W.w[k + 1];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const unsigned i = 2 * k + h;
+      if (i < lo || i >= lim) continue;
+      const unsigned u = h ? cw >> 16 : cw & 0xFFFFu;
+      const unsigned pv = h ? cw & 0xFFFFu : pw >> 16;
+      if (!bytes) {
+        q += is_lo(u) ? 0u : 1u;
+        continue;
+      }
+      unsigned len;
+      const uint32_t p = encode_unit(u, pv, len);
+      if (dst)
+        for (unsigned b = 0; b < len; b++) dst[q + b] = (uint8_t)(p >> (8 * b));
+      q += len;
     }
-    if (dst)
-      for (unsigned b = 0; b < len; b++) dst[q + b] = (uint8_t)(p >> (8 * b));
-    q += len;
+    pw = cw;
   }
   return q;
 }
@@ -195,6 +193,9 @@ struct Class16 {
 };
 
 // Phase A over the 16 own words: pairing check and counts (SWAR, 16-bit lanes).
+// The kernel is bound by the ALU pipe: the surrogate test is one masked XOR and
+// a carry (the add runs on the FMA pipe).  (Summing the flags with IMAD.HI
+// instead of shift + add measured slower: IMAD.HI is quarter rate.)
 __device__ __forceinline__ Class16 classify16(const Words16& W) {
   uint32_t hp;  // high-surrogate plane of the previous word
   {
@@ -206,7 +207,11 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
 #pragma unroll
   for (int k = 1; k <= K16_WPT + 1; k++) {
     const uint32_t x = W.w[k];
-    const uint32_t sr = sur16(x), x5 = x << 5;  // bit 10 (low surrogate) -> bit 15
+    // (t through an asm LOP3: emit_word16_v3 has the same expression, and a
+    // shared value would stay live across the scan and spill)
+    const uint32_t t = lop3<0x6A>(x, 0x78007800u, 0x58005800u);  // (a & b) ^ c: 0 on D800..DFFF
+    const uint32_t sr = lop3<0x20>(x, t + 0x78007800u, H16);  // a & ~b & c
+    const uint32_t x5 = x * 32u;                               // bit 10 (low surrogate) -> 15
     const uint32_t hm = sr & ~x5, lm = sr & x5;
     if (k >= 2) {
       // word k-1: its units' predecessors and successors
@@ -260,7 +265,8 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   const Class16 c = classify16(tc.W);
   unsigned my_err = kNone16;
   if (c.err) {
-    const unsigned er = first_error16(src, tc.v0, tc.lo, hi);
+    const Words16 tmp = tc.W;  // (a copy: tc.W itself stays in registers)
+    const unsigned er = first_error16(tmp, tc.lo, hi);
     if (er != kNone16) my_err = K16_UPT * threadIdx.x + er;
   }
   {
@@ -286,7 +292,10 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
       atomicMin(&a.ctl->err, pos);
     }
   }
-  tc.cnt = generic_units(src, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
+  {
+    const Words16 tmp = tc.W;
+    tc.cnt = generic_units(tmp, tc.lo, tc.lim, kTranscode, nullptr);
+  }
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
@@ -438,7 +447,8 @@ struct Utf16Codec {
       for (int k = 1; k <= K16_WPT; k++) emit_word16_swar(tc.W.w[k], tc.W.w[k - 1], q);
 #endif
     } else {
-      generic_units(Src16{a.base, a.head, a.n, kBE}, tc.v0, tc.lo, tc.lim, true, stage + off);
+      const Words16 tmp = tc.W;
+      generic_units(tmp, tc.lo, tc.lim, true, stage + off);
     }
   }
 };
@@ -488,9 +498,10 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
-      const unsigned er = first_error16(src, v0, lo, hi);
+      const Words16 tmp = W;
+      const unsigned er = first_error16(tmp, lo, hi);
       if (er != kNone16) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
-      cnt = generic_units(src, v0, lo, hi, kUnits, nullptr);
+      cnt = generic_units(tmp, lo, hi, kUnits, nullptr);
     }
     total += cnt;
     const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
@@ -522,7 +533,9 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
       const long long stop = (long long)e + head;
       const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
       const unsigned lim = (unsigned)max((long long)lo, min((long long)K16_UPT, stop - v0));
-      t += generic_units(src, v0, lo, lim, kUnits, nullptr);
+      Words16 tmp;
+      load_edge16<kBE>(src, v0, tmp.w);
+      t += generic_units(tmp, lo, lim, kUnits, nullptr);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);

@@ -59,24 +59,6 @@ struct Words {
   uint32_t w[K8_WPT + 2];  // w[0] = previous word, w[1..16] = own, w[17] = next
 };
 
-__device__ __forceinline__ unsigned byte_at(const Words& W, int p) {  // p in [-4, 68)
-  const int q = p + 4;
-  return (W.w[q >> 2] >> ((q & 3) * 8)) & 0xFFu;
-}
-
-// Byte-granular masked load of a thread's window (ends of the input only).
-__device__ __noinline__ void load_masked(Src a, long long v0, Words& W) {
-  const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
-  for (int k = 0; k < K8_WPT + 2; k++) {
-    uint32_t x = 0;
-    for (int b = 0; b < 4; b++) {
-      const long long p = v0 - 4 + 4 * k + b;
-      if (p >= lo && p < hi) x |= (uint32_t)a.base[p] << (8 * b);
-    }
-    W.w[k] = x;
-  }
-}
-
 // One word straddling an end of the input, byte by byte (rare; out of line).
 __device__ __noinline__ uint32_t straddle_word(Src a, long long p) {
   const long long lo = (long long)a.head, hi = (long long)(a.head + a.n);
@@ -92,6 +74,8 @@ __device__ __noinline__ uint32_t straddle_word(Src a, long long p) {
 // by byte.  Zeros are ASCII to the classification, so an end tile takes the
 // SWAR path like any other (its counts minus the zeros); a character cut by an
 // end, or a continuation byte at the start, still shows as a structure error.
+// (A byte-serial masked load here cost ~70 dependent memory round trips, some
+// 40 us, at the first and the last tile of every call.)
 __device__ __forceinline__ void load_edge(Src a, long long v0, uint32_t* w) {
   constexpr int NW = K8_WPT + 2;
   const long long s0 = v0 - 4;  // virtual position of word 0
@@ -107,25 +91,40 @@ __device__ __forceinline__ void load_edge(Src a, long long v0, uint32_t* w) {
       w[k] = straddle_word(a, s0 + 4 * k);
 }
 
-// Exact first error among positions [lo, hi) of the thread's bytes.  Rare
-// path: reloads the thread's window itself (byte loads), so the hot path keeps
-// its words in registers.
-__device__ __noinline__ unsigned first_error_rule_a(Src a, long long v0, unsigned lo,
-                                                    unsigned hi) {
-  Words W;
-  load_masked(a, v0, W);
-  for (unsigned i = lo; i < hi; i++) {
-    const unsigned b = byte_at(W, (int)i);
-    if ((b & 0xC0u) == 0x80u) {
-      bool covered = false;
-      for (int j = (int)i - 3; j < (int)i; j++)
-        if (leadlen(byte_at(W, j)) > (unsigned)((int)i - j)) covered = true;
-      if (!covered) return i;
-    } else if (b >= 0x80u) {
-      const uint32_t v = b | (byte_at(W, (int)i + 1) << 8) | (byte_at(W, (int)i + 2) << 16) |
-                         (byte_at(W, (int)i + 3) << 24);
-      if (!decode_ok(v)) return i;
+// byte j in [-4, 8) of the 12-byte window (pw, cw, nw) around word cw
+__device__ __forceinline__ unsigned b12(uint32_t pw, uint32_t cw, uint32_t nw, int j) {
+  return j < 0 ? (pw >> (8 * (j + 4))) & 0xFFu : j < 4 ? (cw >> (8 * j)) & 0xFFu
+                                                       : (nw >> (8 * (j - 4))) & 0xFFu;
+}
+
+// Exact first error among positions [lo, hi) of a thread's window (rule A of
+// SURVEY.md 8(a)): the smallest position whose lead fails to decode or whose
+// continuation no lead 1..3 bytes back reaches.  Rare path (tiles with an
+// error), out of line, on a copy of the caller's window (so the hot path keeps
+// its words in registers); one loop step per word with the words before and
+// after in registers.
+__device__ __noinline__ unsigned first_error_w(const Words& W, unsigned lo, unsigned hi) {
+  uint32_t pw = W.w[0], cw = W.w[1];
+  for (int k = 0; k < K8_WPT; k++) {
+    const uint32_t nw = W.w[k + 2];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const unsigned i = 4 * k + j;
+      if (i < lo || i >= hi) continue;
+      const unsigned b = b12(pw, cw, nw, j);
+      if ((b & 0xC0u) == 0x80u) {
+        const bool covered = leadlen(b12(pw, cw, nw, j - 1)) > 1u ||
+                             leadlen(b12(pw, cw, nw, j - 2)) > 2u ||
+                             leadlen(b12(pw, cw, nw, j - 3)) > 3u;
+        if (!covered) return i;
+      } else if (b >= 0x80u) {
+        const uint32_t v = b | (b12(pw, cw, nw, j + 1) << 8) | (b12(pw, cw, nw, j + 2) << 16) |
+                           (b12(pw, cw, nw, j + 3) << 24);
+        if (!decode_ok(v)) return i;
+      }
     }
+    pw = cw;
+    cw = nw;
   }
   return kNone;
 }
@@ -238,36 +237,42 @@ __device__ __forceinline__ uint16_t bswap16(unsigned u) {
   return (uint16_t)(((u & 0xFFu) << 8) | ((u >> 8) & 0xFFu));
 }
 
-__device__ __noinline__ unsigned generic_chars(Src a, long long v0, unsigned lo,
-                                               unsigned lim, bool units, uint16_t* dst,
-                                               bool be = false) {
-  Words W;
-  load_masked(a, v0, W);
+__device__ __noinline__ unsigned generic_chars(const Words& W, unsigned lo, unsigned lim,
+                                               bool units, uint16_t* dst, bool be = false) {
   unsigned q = 0;
-  for (unsigned p = lo; p < lim; p++) {
-    const unsigned b0 = byte_at(W, (int)p);
-    if ((b0 & 0xC0u) == 0x80u) continue;  // continuation
-    const unsigned b1 = byte_at(W, (int)p + 1) & 0x3F, b2 = byte_at(W, (int)p + 2) & 0x3F,
-                   b3 = byte_at(W, (int)p + 3) & 0x3F;
-    unsigned cp;
-    if (b0 < 0x80u) cp = b0;
-    else if (b0 < 0xE0u) cp = ((b0 & 0x1Fu) << 6) | b1;
-    else if (b0 < 0xF0u) cp = ((b0 & 0x0Fu) << 12) | (b1 << 6) | b2;
-    else cp = ((b0 & 0x07u) << 18) | (b1 << 12) | (b2 << 6) | b3;
-    if (!units) {
-      q++;
-    } else if (cp < 0x10000u) {
-      if (dst) dst[q] = be ? bswap16(cp) : (uint16_t)cp;
-      q++;
-    } else {
-      const unsigned s = cp - 0x10000u;
-      if (dst) {
-        const unsigned h = 0xD800u + (s >> 10), l = 0xDC00u + (s & 0x3FFu);
-        dst[q] = be ? bswap16(h) : (uint16_t)h;
-        dst[q + 1] = be ? bswap16(l) : (uint16_t)l;
+  uint32_t pw = W.w[0], cw = W.w[1];
+  for (int k = 0; k < K8_WPT; k++) {
+    const uint32_t nw = W.w[k + 2];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const unsigned p = 4 * k + j;
+      if (p < lo || p >= lim) continue;
+      const unsigned b0 = b12(pw, cw, nw, j);
+      if ((b0 & 0xC0u) == 0x80u) continue;  // continuation
+      const unsigned b1 = b12(pw, cw, nw, j + 1) & 0x3F, b2 = b12(pw, cw, nw, j + 2) & 0x3F,
+                     b3 = b12(pw, cw, nw, j + 3) & 0x3F;
+      unsigned cp;
+      if (b0 < 0x80u) cp = b0;
+      else if (b0 < 0xE0u) cp = ((b0 & 0x1Fu) << 6) | b1;
+      else if (b0 < 0xF0u) cp = ((b0 & 0x0Fu) << 12) | (b1 << 6) | b2;
+      else cp = ((b0 & 0x07u) << 18) | (b1 << 12) | (b2 << 6) | b3;
+      if (!units) {
+        q++;
+      } else if (cp < 0x10000u) {
+        if (dst) dst[q] = be ? bswap16(cp) : (uint16_t)cp;
+        q++;
+      } else {
+        const unsigned s = cp - 0x10000u;
+        if (dst) {
+          const unsigned h = 0xD800u + (s >> 10), l = 0xDC00u + (s & 0x3FFu);
+          dst[q] = be ? bswap16(h) : (uint16_t)h;
+          dst[q + 1] = be ? bswap16(l) : (uint16_t)l;
+        }
+        q += 2;
       }
-      q += 2;
     }
+    pw = cw;
+    cw = nw;
   }
   return q;
 }
@@ -438,7 +443,8 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   tc.lim = hi;
   unsigned my_err = kNone;
   if (co.viol) {
-    const unsigned er = first_error_rule_a(src, tc.v0, tc.lo, hi);
+    const Words tmp = tc.W;  // (a copy: tc.W itself stays in registers)
+    const unsigned er = first_error_w(tmp, tc.lo, hi);
     if (er != kNone) my_err = K8_BPT * threadIdx.x + er;
   }
   {
@@ -467,7 +473,10 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
       atomicMin(&a.ctl->err, pos);
     }
   }
-  tc.cnt = generic_chars(src, tc.v0, tc.lo, tc.lim, kTranscode, nullptr);
+  {
+    const Words tmp = tc.W;
+    tc.cnt = generic_chars(tmp, tc.lo, tc.lim, kTranscode, nullptr);
+  }
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
@@ -496,7 +505,8 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
 #endif
     }
   } else {
-    generic_chars(Src{a.base, a.head, a.n}, tc.v0, tc.lo, tc.lim, true, stage + off, kBE);
+    const Words tmp = tc.W;
+    generic_chars(tmp, tc.lo, tc.lim, true, stage + off, kBE);
   }
 }
 
@@ -584,9 +594,10 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
-      const unsigned er = first_error_rule_a(src, v0, lo, hi);
+      const Words tmp = W;
+      const unsigned er = first_error_w(tmp, lo, hi);
       if (er != kNone) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
-      cnt = generic_chars(src, v0, lo, hi, kUnits, nullptr);
+      cnt = generic_chars(tmp, lo, hi, kUnits, nullptr);
     }
     total += cnt;
     const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
@@ -620,7 +631,9 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
       const long long stop = (long long)e + head;
       const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
       const unsigned lim = (unsigned)max((long long)lo, min((long long)K8_BPT, stop - v0));
-      t += generic_chars(src, v0, lo, lim, kUnits, nullptr);
+      Words tmp;
+      load_edge(src, v0, tmp.w);
+      t += generic_chars(tmp, lo, lim, kUnits, nullptr);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);

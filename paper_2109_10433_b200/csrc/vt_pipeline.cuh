@@ -249,17 +249,6 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         // (the error word was read at the top of the tile: one round trip
         // less on the path every warp waits for at the loop-top barrier)
         unsigned t = atomicAdd(&a.ctl->tile_counter, 1u);
-#ifdef VT_PREFETCH
-        {  // experiment: ask L2 for the input of the tile taken ~one round later
-          constexpr unsigned kEB = sizeof(*a.base);
-          const unsigned long long pt = (unsigned long long)t + VT_PREFETCH * gridDim.x;
-          if (pt + 1 < a.ntiles)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                             reinterpret_cast<const char*>(a.base) + pt * C::kTileElems * kEB),
-                         "r"(C::kTileElems * kEB)
-                         : "memory");
-        }
-#endif
         if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
           t = a.ntiles;
         sm.tile = t;
