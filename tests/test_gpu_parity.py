@@ -119,6 +119,55 @@ def test_lengths_and_offsets_utf16(oracle, torch):
             assert (out[:ooff].cpu().numpy() == 0xEE).all()
 
 
+def test_end_tiles(oracle, torch):
+    """The first and last tile of a multi-tile input take the SWAR path on a
+    masked window (zeros outside the input): valid text, an error in the first
+    or last bytes, a 4-byte character ending exactly at the input end, at every
+    start offset 0..15 and a spread of lengths around tile sizes."""
+    rng = np.random.default_rng(7)
+    body = _gen_text(rng, 30000, (40, 20, 30, 10)).encode()
+    buf = torch.zeros(len(body) + 64, dtype=torch.uint8, device="cuda")
+    o16 = torch.zeros(len(body) + 64, dtype=torch.int16, device="cuda")
+    four = "\U0001F600".encode()
+    for ln in (16384 + 5, 32768 - 3, 40000, 65536 + 64):
+        base = bytearray(body[:ln])
+        while base and (base[-1] & 0xC0) == 0x80:  # whole characters
+            base.pop()
+        cases = [bytes(base), b"\x80" + bytes(base[1:]), bytes(base[:-1]) + b"\xe9",
+                 bytes(base[:-4]) + four, b"\xf0\x9f" + bytes(base[2:])]
+        for data in cases:
+            want_out, want = oracle.utf8_to_utf16(data)
+            for off in (0, 1, 7, 15):
+                arr = np.zeros(buf.numel(), dtype=np.uint8)
+                arr[off:off + len(data)] = np.frombuffer(data, dtype=np.uint8)
+                buf.copy_(torch.from_numpy(arr))
+                r = vt.utf8_to_utf16_device(buf, len(data), o16, offset=off)
+                assert _same(r, want), (ln, off, data[:2].hex(), data[-2:].hex())
+                got = o16[: r.written].cpu().numpy().view(np.uint16)
+                assert np.array_equal(got, want_out), (ln, off)
+                assert vt.validate_utf8_device(buf, len(data), offset=off).error_at == want.error_at
+    units = np.frombuffer(_gen_text(rng, 30000, (40, 20, 30, 10)).encode("utf-16-le"), dtype=np.uint16)
+    b16 = torch.zeros(units.size + 64, dtype=torch.int16, device="cuda")
+    o8 = torch.zeros(3 * units.size + 64, dtype=torch.uint8, device="cuda")
+    for ln in (8192 + 3, 16384 - 1, 20000):
+        u = units[:ln].copy()
+        if 0xD800 <= u[-1] <= 0xDBFF:
+            u = u[:-1]
+        lone_lo = u.copy(); lone_lo[0] = 0xDC00
+        cut_hi = u.copy(); cut_hi[-1] = 0xD83D
+        pair_end = u.copy(); pair_end[-2], pair_end[-1] = 0xD83D, 0xDE00
+        for uu in (u, lone_lo, cut_hi, pair_end):
+            want_out, want = oracle.utf16_to_utf8(uu)
+            for off in (0, 1, 7):
+                arr = np.zeros(b16.numel(), dtype=np.uint16)
+                arr[off:off + uu.size] = uu
+                b16.copy_(torch.from_numpy(arr.view(np.int16)))
+                r = vt.utf16_to_utf8_device(b16, uu.size, o8, offset=2 * off)
+                assert _same(r, want), (ln, off, hex(uu[0]), hex(uu[-1]))
+                assert np.array_equal(o8[: r.written].cpu().numpy(), want_out), (ln, off)
+                assert vt.validate_utf16_device(b16, uu.size, offset=2 * off).error_at == want.error_at
+
+
 # ---- tile / row / thread seams ------------------------------------------------------
 
 SEAMS = [0, 1, 2, 3, 15, 16, 17, 4093, 4094, 4095, 4096, 4097, 8189, 8190, 8191, 8192, 8193,

@@ -3,7 +3,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
 import paper_2109_10433_b200 as vt
 L = vt.lib(); L.vt_debug_probe.argtypes = [C.c_void_p, C.c_void_p]
-d, n, _ = vt.generate(2, 1 << 30)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+d, n, _ = vt.generate(cfg, 1 << 30)
 o = torch.empty(n + 8, dtype=torch.int16, device="cuda")
 res = torch.zeros(3, dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream()
