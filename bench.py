@@ -205,6 +205,22 @@ def run_reference_arm(args, rank):
     }
 
 
+def timed_steps_flushed(step, steps, stream, flush, torch):
+    """Device time (ms) of `steps` calls, each bracketed by its own events on the
+    launching stream, with an L2 flush (a write of a buffer larger than L2)
+    between the calls and outside the events."""
+    evs = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -272,6 +288,11 @@ def main():
             vt.utf16_to_utf8_device(d16, n16, d_out, stream=stream, d_res=d_res2)
         kernel = "vt::utf8_transcode_kernel + vt::utf16_transcode_kernel"
 
+    # inputs that fit the 126 MB L2 (cfg1), or of which a call reads only the
+    # prefix up to its first error (cfg4, ~16 MB): L2 flushed between timed
+    # steps by writing a buffer larger than L2, outside the per-step events
+    flush = (torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+             if in_bytes < (256 << 20) or args.config == 4 else None)
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
             step()
@@ -284,16 +305,19 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = vt.launch_count()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+        else:
+            ms = timed_steps_flushed(step, args.steps, stream, flush, torch)
         launches = vt.launch_count() - launches0
         if dist:
             dist.barrier()
-        ms = e0.elapsed_time(e1)
     res = vt.result_from_device(d_res)
     if kind == "rt":
         res2 = vt.result_from_device(d_res2)
@@ -358,8 +382,9 @@ def main():
         "data": "synthetic (seeded splitmix64 chunk generator in HBM, BASELINE cfg shape; corpora absent)",
         "config": {"workload": desc, "input_bytes_per_gpu": in_bytes, "output_elems_per_gpu": res.written,
                    "chars_total": chars,
-                   "l2": ("input > 126 MB L2: no flush between steps" if in_bytes > (256 << 20)
-                          else "input fits L2: steps re-read it from L2 (cfg1 is launch-latency bound)"),
+                   "l2": ("input > 126 MB L2: no flush between steps" if flush is None
+                          else "L2 flushed (512 MiB write) between timed steps, each step timed "
+                               "by its own events (the bytes a call reads fit L2)"),
                    "parallelism": f"shards x{world} (no collective)" if world > 1 else "single GPU"},
         "gchars_per_s": round(chars / (per_step_ms / 1e3) / 1e9, 2),
         "result": {"consumed": gres.consumed, "written": gres.written, "error_at": gres.error_at},
@@ -376,13 +401,17 @@ def main():
         vres = torch.zeros(3, dtype=torch.int64, device="cuda")
         for _ in range(3):
             vfn(d_in, n, stream=stream, d_res=vres)
-        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        v0.record(stream)
-        for _ in range(args.steps):
-            vfn(d_in, n, stream=stream, d_res=vres)
-        v1.record(stream)
-        torch.cuda.synchronize()
-        vms = v0.elapsed_time(v1) / args.steps
+        if flush is None:
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(args.steps):
+                vfn(d_in, n, stream=stream, d_res=vres)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            vms = v0.elapsed_time(v1) / args.steps
+        else:
+            vms = timed_steps_flushed(lambda: vfn(d_in, n, stream=stream, d_res=vres), args.steps,
+                                      stream, flush, torch) / args.steps
         vbytes = in_bytes if res.error_at is None else (2 if kind == "u16" else 1) * res.error_at
         line["validate"] = {"kernel": "vt::utf16_validate_rows_kernel" if kind == "u16"
                             else "vt::utf8_validate_rows_kernel",
