@@ -105,14 +105,21 @@ __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p
 // them newest first: a fully-ready window without an inclusive prefix is summed
 // and passed, the first window with a prefix ends the walk.  A window that is
 // not ready yet stops the step; the ready part before it is banked and the step
-// repeats from there.  When the prefix is found the warp also publishes the
-// inclusive prefixes of every aggregate-only tile it summed in this step
-// ("helping"), so the prefix frontier keeps up with the tiles in flight.
+// repeats from there.  The caller publishes the tile's own inclusive prefix
+// (with VT_LB_HELP also those of the aggregate-only tiles summed: "helping").
 //
 // Aggregates are tile-sized (< 2^16 elements, <= 3 output bytes each), so sums
 // over one step's <= 32 * VT_LB_WIN tiles fit in 32 bits (32-bit shuffles, REDUX).
 #ifndef VT_LB_WIN
 #define VT_LB_WIN 1  // measured: 2 and 4 windows per step are slower (L2 contention)
+#endif
+// VT_LB_HELP: a look-back also publishes the inclusive prefixes of the
+// aggregate-only tiles it summed.  Off: concurrent look-backs walking the same
+// tiles stored the same prefixes to the hottest status lines, which every
+// poller and publisher hits (measured without: 0.910 -> 0.901 ms cfg2, 1.234 ->
+// 1.231 cfg3, 12.16 -> 12.13 cfg5).
+#ifndef VT_LB_HELP
+#define VT_LB_HELP 0
 #endif
 #ifndef VT_LB_DELAY
 #define VT_LB_DELAY 3000  // ns before the first poll
@@ -168,7 +175,8 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
           if (lane + o < 32) x += y;
         }
         if (lane < stop)
-          store_status(&status[base - 32 * kk - lane], pack_status(kFlagPre, epoch, pval + x));
+          if (VT_LB_HELP)
+            store_status(&status[base - 32 * kk - lane], pack_status(kFlagPre, epoch, pval + x));
         unsigned long long newer = pval + __shfl_sync(0xffffffffu, x, 0);  // prefix through window k
         // windows k-1 .. 0 (fully ready, summed): their tiles' inclusive prefixes
 #pragma unroll
@@ -179,7 +187,8 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
             const uint32_t y = __shfl_down_sync(0xffffffffu, z, o);
             if (lane + o < 32) z += y;
           }
-          store_status(&status[base - 32 * j - lane], pack_status(kFlagPre, epoch, newer + z));
+          if (VT_LB_HELP)
+            store_status(&status[base - 32 * j - lane], pack_status(kFlagPre, epoch, newer + z));
           newer += wsum[j];
         }
         return excl + newer;
