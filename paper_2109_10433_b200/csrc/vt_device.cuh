@@ -62,11 +62,14 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 
 // Per-call control block.  Zeroed once at allocation; the finalising CTA of
 // every launch re-arms it, so consecutive calls on one stream need no memset.
+// The tile counter takes one atomic per tile from every CTA: it has a 128-byte
+// line to itself, so the error word every tile reads is not queued behind it.
 struct Ctl {
-  unsigned int tile_counter;
-  unsigned int done;
+  alignas(128) unsigned int tile_counter;
+  unsigned int line_pad[31];
   unsigned long long err;    // smallest failing input index seen, kNoError if none
   unsigned long long count;  // validate/count kernels: code points in the valid prefix
+  unsigned int done;
   unsigned long long pad[5];
 };
 
