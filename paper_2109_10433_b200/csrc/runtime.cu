@@ -187,7 +187,6 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
     return e ? (unsigned)std::strtoul(e, nullptr, 0) : 0u;
   }();
   a.dbg = dbg;
-  a.k = vt::shr_k();
   a.skip = d_skip;
   a.rows = nullptr;
   if (!transcode) {

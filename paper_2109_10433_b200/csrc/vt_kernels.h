@@ -14,15 +14,6 @@ struct Ctl;
 
 // UTF-8 side: `base` is the input rounded down to 16 bytes, `head` the offset
 // of the first input byte from it.  Tiles cover virtual bytes [0, head + n).
-// Right shifts as multiplies: x >> s == umulhi(x, 2^(32-s)).  The kernels are
-// bound by the ALU pipe (LOP3/PRMT/SHF, half rate) while the FMA pipe (IMAD,
-// full rate) idles, so hot shifts go through IMAD.HI.  The multipliers come
-// from the kernel parameters so the compiler cannot fold them back into shifts;
-// the host always fills them with shr_k().
-struct ShrK {
-  unsigned s2, s7, s8, s16;  // 2^30, 2^25, 2^24, 2^16
-};
-inline ShrK shr_k() { return ShrK{1u << 30, 1u << 25, 1u << 24, 1u << 16}; }
 
 struct U8Args {
   const uint8_t* base;
@@ -35,7 +26,6 @@ struct U8Args {
   Ctl* ctl;
   vt_result* res;
   unsigned dbg;  // debug switches (VT_DEBUG env), 0 in production
-  ShrK k;
   const unsigned* skip;  // validate only: device count of leading bytes to skip, or null
   unsigned* rows;        // validate only: per-row counts scratch (rows_utf8 entries)
 };
