@@ -103,7 +103,7 @@ __device__ __forceinline__ bool is_lo(unsigned u) { return (u & 0xFC00u) == 0xDC
 
 // UTF-8 bytes written for the unit u (little-endian in the result) and their
 // number; `pv` is the unit before it.  A surrogate pair's 4 bytes are split
-// 2 + 2 between its halves (see emit_word16_swar), so each unit writes 1-3
+// 2 + 2 between its halves (see emit_word16_v3), so each unit writes 1-3
 // bytes and a pair may straddle threads and tiles.
 __device__ __forceinline__ uint32_t encode_unit(unsigned u, unsigned pv, unsigned& len) {
   if (u < 0x80u) {
@@ -304,50 +304,9 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
 // 2 + 2 between its halves -- with w = (hi & 0x3FF) + 0x40 (code point bits
 // 10..20), the high half writes F0|w>>8, 80|(w>>2)&3F and the low half writes
 // 80|(w&3)<<4|(lo>>6)&0xF, 80|lo&3F, where w & 3 == hi & 3.  So no lane needs
-// its neighbour except for two bits of the previous unit.  px: previous word.
-__device__ __forceinline__ void emit_word16_swar(uint32_t x, uint32_t px, uint32_t& q) {
-  // (no ASCII-pair shortcut: in mixed warps it runs beside the full form;
-  // measured slower even on 90 % ASCII)
-  // (the shared-plane forms of classify16 spill here: measured slower)
-  const uint32_t g80 = (((x & 0xFF80FF80u) >> 1) + 0x7FC07FC0u) & H16;   // u >= 0x80
-  const uint32_t g800 = (((x & 0xF800F800u) >> 1) + 0x7C007C00u) & H16;  // u >= 0x800
-  const uint32_t sur = ~nz_hi6((x & 0xF800F800u) ^ 0xD800D800u) & H16;   // D800..DFFF
-  const uint32_t hs = ~nz_hi6((x & 0xFC00FC00u) ^ 0xD800D800u) & H16;    // D800..DBFF
-  const uint32_t is3 = g800 & ~sur;
-  // full 16-bit lane masks (PRMT sign replication of bytes 1 and 3)
-  const uint32_t m80 = prmt(g80, 0, 0xBB99), m3 = prmt(is3, 0, 0xBB99);
-  const uint32_t ms = prmt(sur, 0, 0xBB99), mh = prmt(hs, 0, 0xBB99);
-  const uint32_t c6 = x & 0x003F003Fu;
-  const uint32_t b6 = (x >> 6) & 0x003F003Fu;
-  const uint32_t a4 = (x >> 12) & 0x000F000Fu;
-  const uint32_t w = (x & 0x03FF03FFu) + 0x00400040u;
-  const uint32_t pu = __funnelshift_l(px, x, 16);  // previous unit of each lane
-  // first byte
-  const uint32_t f_lo = 0x00800080u | ((pu & 0x00030003u) << 4) | (b6 & 0x000F000Fu);
-  const uint32_t f_hi = 0x00F000F0u | (w >> 8);
-  const uint32_t f_sur = (f_hi & mh) | (f_lo & ~mh);
-  const uint32_t f_bmp = (m3 & (0x00E000E0u | a4)) | (~m3 & (0x00C000C0u | b6));
-  uint32_t F = (ms & f_sur) | (~ms & f_bmp);
-  F = (m80 & F) | (~m80 & x);
-  // second and third bytes
-  const uint32_t s_hi = (w >> 2) & 0x003F003Fu;
-  const uint32_t S = 0x00800080u | (m3 & b6) | (mh & s_hi) | (~(m3 | mh) & c6);
-  const uint32_t T = 0x00800080u | c6;
-  // per-lane length 1..3
-  const uint32_t n = 0x00010001u + (g80 >> 15) + (is3 >> 15);
-  const uint32_t n0 = n & 0xFFFFu, n1 = n >> 16;
-  sts8(q, F);
-  if (n0 >= 2) sts8(q + 1, S);
-  if (n0 == 3) sts8(q + 2, T);
-  q += n0;
-  sts8(q, F >> 16);
-  if (n1 >= 2) sts8(q + 1, S >> 16);
-  if (n1 == 3) sts8(q + 2, T >> 16);
-  q += n1;
-}
-
-// Same bytes as emit_word16_swar, with fewer ALU-pipe instructions (the kernel
-// is bound by the ALU pipe; IMAD and IADD go to the FMA pipe):
+// its neighbour except for two bits of the previous unit (px: previous word).
+// Written for few ALU-pipe instructions (the kernel is bound by the ALU pipe;
+// IMAD and IADD go to the FMA pipe):
 //  * only the low byte of each 16-bit lane has to be right (sts8 stores the
 //    low byte), so most masks after right shifts disappear;
 //  * the surrogate test is one masked XOR and a carry (no shift);
@@ -411,9 +370,6 @@ __device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t
   q = q1 + (n >> 16);
 }
 
-#ifndef VT_U16_EMIT
-#define VT_U16_EMIT 3
-#endif
 #ifndef VT_NSTAGE16
 #define VT_NSTAGE16 1  // two buffers: 1.375 vs 1.370 ms on cfg3 (with the L1 they take away)
 #endif
@@ -438,14 +394,9 @@ struct Utf16Codec {
       // (tc.lo > 0 only for the first thread of a call: the zeros before the
       // input are encoded too and land in the pad before the staging buffer)
       uint32_t q = smem_addr(stage) + off - tc.lo;
-#if VT_U16_EMIT == 3
 #pragma unroll
       for (int k = 1; k < K16_WPT; k++) emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q);
       emit_word16_v3<false>(tc.W.w[K16_WPT], tc.W.w[K16_WPT - 1], q);
-#else
-#pragma unroll
-      for (int k = 1; k <= K16_WPT; k++) emit_word16_swar(tc.W.w[k], tc.W.w[k - 1], q);
-#endif
     } else {
       const Words16 tmp = tc.W;
       generic_units(tmp, tc.lo, tc.lim, true, stage + off);

@@ -38,9 +38,6 @@ constexpr int K8_WPT = VT_K8_WPT;               // words per thread
 constexpr int K8_BPT = 4 * K8_WPT;              // bytes per thread
 constexpr int K8_TILE = K8_THREADS * K8_BPT;    // bytes per tile
 constexpr unsigned kNone = 0xFFFFFFFFu;
-#ifndef VT_FOUR_EMIT
-#define VT_FOUR_EMIT 2  // 1: separate low-surrogate stores (8 per word)
-#endif
 constexpr uint32_t H = 0x80808080u;
 
 __device__ __forceinline__ unsigned leadlen(unsigned b) {
@@ -281,9 +278,9 @@ __device__ __noinline__ unsigned generic_chars(const Words& W, unsigned lo, unsi
 }
 
 // Branch-free decode of one word: lead-attributed byte planes of each
-// character's UTF-16 unit (BMP), plus, with kFour, the surrogate pair of
-// 4-byte characters.  Predicated 16-bit stores at the running offset q.
-template <bool kFour, bool kBE>
+// character's UTF-16 unit (BMP only; words with 4-byte characters take
+// emit_word_four).  Predicated 16-bit stores at the running offset q.
+template <bool kBE>
 __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
@@ -300,41 +297,12 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t him = ((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3);
   const uint32_t hi = him & mna;
   // units of lanes 0,1 and 2,3 (little-endian; UTF-16BE swaps the two bytes)
-  uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140), u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
-  if (!kFour) {
-    if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
-    if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
-    if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
-    if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
-  } else {
-    // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10), low = 0xDC00 | (cp & 0x3FF)
-    const uint32_t n3 = prmt(c, n, 0x6543);
-    const uint32_t four7 = ge_e0 & (c << 3) & H;
-    const uint32_t m4 = prmt(four7, 0, 0xBA98);
-    const uint32_t X = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
-    const uint32_t c7 = c & 0x07070707u;
-    uint32_t hs01 = prmt(X, c7, 0x5140) + 0xD7C0D7C0u;
-    uint32_t hs23 = prmt(X, c7, 0x7362) + 0xD7C0D7C0u;
-    const uint32_t lsl = ((n2 << 6) & 0xC0C0C0C0u) | (n3 & 0x3F3F3F3Fu);
-    const uint32_t lsh = ((n2 >> 2) & 0x03030303u) | 0xDCDCDCDCu;
-    const uint32_t ls01 = prmt(lsl, lsh, kBE ? 0x1504 : 0x5140);
-    const uint32_t ls23 = prmt(lsl, lsh, kBE ? 0x3726 : 0x7362);
-    if (kBE) {
-      hs01 = prmt(hs01, 0, 0x2301);
-      hs23 = prmt(hs23, 0, 0x2301);
-    }
-    const uint32_t m4_01 = prmt(m4, 0, 0x1100), m4_23 = prmt(m4, 0, 0x3322);
-    u01 = (u01 & ~m4_01) | (hs01 & m4_01);
-    u23 = (u23 & ~m4_23) | (hs23 & m4_23);
-    if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
-    if (four7 & 0x00000080u) { sts16(q, ls01); q += 2; }
-    if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
-    if (four7 & 0x00008000u) { sts16(q, (ls01 >> 16)); q += 2; }
-    if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
-    if (four7 & 0x00800000u) { sts16(q, ls23); q += 2; }
-    if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
-    if (four7 & 0x80000000u) { sts16(q, (ls23 >> 16)); q += 2; }
-  }
+  const uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140);
+  const uint32_t u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
+  if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
+  if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
+  if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
+  if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
 }
 
 // Words with 4-byte characters: one unit per lane, like the BMP form.  A
@@ -495,17 +463,12 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
     // per-thread choice would run both forms in mixed warps
     if (!__any_sync(0xffffffffu, tc.four)) {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<false, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) emit_word<kBE>(tc.W.w[k], tc.W.w[k + 1], q);
     } else {
-#if VT_FOUR_EMIT == 2
       uint32_t carry4 = 0;  // a lead in the previous thread finishes its own pair
 #pragma unroll
       for (int k = 1; k <= K8_WPT; k++) emit_word_four<kBE>(tc.W.w[k], tc.W.w[k + 1], q, carry4);
       if (carry4) emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
-#else
-#pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<true, kBE>(tc.W.w[k], tc.W.w[k + 1], q);
-#endif
     }
   } else {
     const Words tmp = tc.W;
