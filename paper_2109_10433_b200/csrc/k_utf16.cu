@@ -204,12 +204,14 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
   }
   uint32_t hcur = 0, lcur = 0;
   uint32_t err = 0, acc = 0, nlo = 0, nsur = 0;
+  // (0x58005800 in an opaque register, as in the emit, measured +-0 here)
+  constexpr uint32_t K58 = 0x58005800u;
 #pragma unroll
   for (int k = 1; k <= K16_WPT + 1; k++) {
     const uint32_t x = W.w[k];
     // (t through an asm LOP3: emit_word16_v3 has the same expression, and a
     // shared value would stay live across the scan and spill)
-    const uint32_t t = lop3<0x6A>(x, 0x78007800u, 0x58005800u);  // (a & b) ^ c: 0 on D800..DFFF
+    const uint32_t t = lop3<0x6A>(x, 0x78007800u, K58);  // (a & b) ^ c: 0 on D800..DFFF
     const uint32_t sr = lop3<0x20>(x, t + 0x78007800u, H16);  // a & ~b & c
     const uint32_t x5 = x * 32u;                               // bit 10 (low surrogate) -> 15
     const uint32_t hm = sr & ~x5, lm = sr & x5;
@@ -316,14 +318,15 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
 //    order).  Only the thread's last word may not spill (the bytes after it
 //    belong to the next thread): it takes the predicated form.
 template <bool kOverlap>
-__device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t& q) {
+__device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t& q, uint32_t K80,
+                                               uint32_t KE0, uint32_t K58) {
   // (x15 through an asm LOP3: classify16 computes the same compare planes, and
   // if the compiler shares them they stay live across the scan and spill)
   const uint32_t x15 = lop3<0xC0>(x, 0x7FFF7FFFu, 0u);
   const uint32_t g80 = lop3<0xA8>(x15 + 0x7F807F80u, x, H16);    // u >= 0x80
   const uint32_t g800 = lop3<0xA8>(x15 + 0x78007800u, x, H16);   // u >= 0x800
   // D800..DFFF: bit 15 set and bits 11..14 == 1011
-  const uint32_t t = (x & 0x78007800u) ^ 0x58005800u;
+  const uint32_t t = lop3<0x6A>(x, 0x78007800u, K58);            // (a & b) ^ c
   const uint32_t sur = lop3<0x20>(x, t + 0x78007800u, H16);       // a & ~b & c
   const uint32_t hs = sur & ~(x * 32u);                           // bit 10 clear: high
   const uint32_t is3 = g800 & ~sur;
@@ -339,20 +342,18 @@ __device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t
   uint32_t F1;
   {
     const uint32_t F2 = x6 | 0x00C000C0u;
-    const uint32_t F3 = ((x >> 12) & 0x000F000Fu) | 0x00E000E0u;
+    const uint32_t F3 = lop3<0xEA>(x >> 12, 0x000F000Fu, KE0);      // (a & b) | c
     const uint32_t Fh = (w >> 8) | 0x00F000F0u;
     const uint32_t pu16 = prmt(px, x, 0x5432) * 16u;                // previous unit << 4
-    const uint32_t Fl = (lop3<0xCA>(0x000F000Fu, x6, pu16) & 0x003F003Fu) | 0x00800080u;
+    const uint32_t Fl = lop3<0xEA>(lop3<0xCA>(0x000F000Fu, x6, pu16), 0x003F003Fu, K80);
     // selections (mux(m, a, b) = m ? a : b, LOP3 0xCA with the mask first)
     const uint32_t Fn = lop3<0xCA>(ms, lop3<0xCA>(mh, Fh, Fl), lop3<0xCA>(m3, F3, F2));
     const uint32_t F = lop3<0xCA>(m80, Fn, x);
     sts8(q, F);
     F1 = F >> 16;
   }
-  const uint32_t T = (x & 0x003F003Fu) | 0x00800080u;
-  const uint32_t S3 = (x6 & 0x003F003Fu) | 0x00800080u;
-  const uint32_t Sh = ((w >> 2) & 0x003F003Fu) | 0x00800080u;
-  const uint32_t S = lop3<0xCA>(m3, S3, lop3<0xCA>(mh, Sh, T));
+  const uint32_t T = lop3<0xEA>(x, 0x003F003Fu, K80);
+  const uint32_t S = lop3<0xEA>(lop3<0xCA>(m3, x6, lop3<0xCA>(mh, w >> 2, x)), 0x003F003Fu, K80);
   if (kOverlap) {
     sts8(q + 1, S);
     sts8(q + 2, T);
@@ -388,16 +389,34 @@ struct Utf16Codec {
                                                unsigned& agg) {
     count_tile16<kTranscode, NT, Sync, kBE>(a, tile, red, scan, tc, off, agg);
   }
+  template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
-                                              unsigned off) {
+                                              unsigned off, Mid&& mid) {
     if (tc.simple) {
       // (tc.lo > 0 only for the first thread of a call: the zeros before the
       // input are encoded too and land in the pad before the staging buffer)
       uint32_t q = smem_addr(stage) + off - tc.lo;
+      // constants or'ed in after a mask, in registers: LOP3 takes one
+      // immediate, so "(v & imm) | K" is one instruction only with K in a
+      // register (opaque, or ptxas folds it back into two)
+      uint32_t K80 = 0x00800080u, KE0 = 0x00E000E0u, K58 = 0x58005800u;
+      asm volatile("" : "+r"(K80), "+r"(KE0), "+r"(K58));
 #pragma unroll
-      for (int k = 1; k < K16_WPT; k++) emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q);
-      emit_word16_v3<false>(tc.W.w[K16_WPT], tc.W.w[K16_WPT - 1], q);
+      for (int k = 1; k < K16_WPT; k++) {
+        if (k == VT_GRAB_AT_U16 + 1) {
+          mid();
+          __syncwarp();  // (keeps ptxas from sinking the atomic behind the stores)
+        }
+        emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q, K80, KE0, K58);
+      }
+      if (VT_GRAB_AT_U16 == K16_WPT - 1) {
+        mid();
+        __syncwarp();
+      }
+      emit_word16_v3<false>(tc.W.w[K16_WPT], tc.W.w[K16_WPT - 1], q, K80, KE0, K58);
+      if (VT_GRAB_AT_U16 >= K16_WPT) mid();
     } else {
+      mid();
       const Words16 tmp = tc.W;
       generic_units(tmp, tc.lo, tc.lim, true, stage + off);
     }

@@ -292,7 +292,7 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t m3 = prmt(ge_e0, 0, 0xBA98);
   const uint32_t A = (n1 & m3) | (c & ~m3);            // 3-byte: 2nd byte; 2-byte: lead
   const uint32_t B = (n2 & m3) | (n1 & ~m3);           // last byte of the character
-  const uint32_t lom = ((A << 6) & 0xC0C0C0C0u) | (B & 0x3F3F3F3Fu);
+  const uint32_t lom = lop3<0xE2>(B, 0x3F3F3F3Fu, A << 6);       // (a & b) | (c & ~b)
   const uint32_t lo = (c & ~mna) | (lom & mna);
   const uint32_t him = ((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3);
   const uint32_t hi = him & mna;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
 // ls lane in the next thread and is finished by emit_tail_ls.
 template <bool kBE>
 __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t& q,
-                                               uint32_t& carry4) {
+                                               uint32_t& carry4, uint32_t KDC) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
   const uint32_t c2 = c << 1;
@@ -330,10 +330,10 @@ __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t&
   const uint32_t mls = prmt(ls7, 0, 0xBA98);
   const uint32_t A = (n1 & m3) | (c & ~m3);
   const uint32_t B = (n2 & m3) | (n1 & ~m3);
-  const uint32_t lom = ((A << 6) & 0xC0C0C0C0u) | (B & 0x3F3F3F3Fu);
+  const uint32_t lom = lop3<0xE2>(B, 0x3F3F3F3Fu, A << 6);       // (a & b) | (c & ~b)
   const uint32_t lo = (c & ~mna) | (lom & mna);
   const uint32_t him = (((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3)) & mna;
-  const uint32_t hi_ls = ((n1 >> 2) & 0x03030303u) | 0xDCDCDCDCu;
+  const uint32_t hi_ls = lop3<0xEA>(n1 >> 2, 0x03030303u, KDC);  // (a & b) | c
   const uint32_t hi = lop3<0xCA>(mls, hi_ls, him);
   uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140), u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
   // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10)
@@ -452,9 +452,9 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
 }
 
 // ---- per-tile back half: decode into the staging buffer -----------------------
-template <bool kBE>
+template <bool kBE, class Mid>
 __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
-                                          unsigned off) {
+                                          unsigned off, Mid&& mid) {
   if (tc.simple) {
     // (tc.lo > 0 only for the first thread of a call: the zeros before the
     // input are decoded too and land in the pad before the staging buffer)
@@ -463,14 +463,25 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
     // per-thread choice would run both forms in mixed warps
     if (!__any_sync(0xffffffffu, tc.four)) {
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word<kBE>(tc.W.w[k], tc.W.w[k + 1], q);
+      for (int k = 1; k <= K8_WPT; k++) {
+        if (k == VT_GRAB_AT_U8 + 1) mid();
+        emit_word<kBE>(tc.W.w[k], tc.W.w[k + 1], q);
+      }
+      if (VT_GRAB_AT_U8 >= K8_WPT) mid();
     } else {
       uint32_t carry4 = 0;  // a lead in the previous thread finishes its own pair
+      uint32_t KDC = 0xDCDCDCDCu;  // in a register: "(v & imm) | KDC" is one LOP3
+      asm volatile("" : "+r"(KDC));
 #pragma unroll
-      for (int k = 1; k <= K8_WPT; k++) emit_word_four<kBE>(tc.W.w[k], tc.W.w[k + 1], q, carry4);
+      for (int k = 1; k <= K8_WPT; k++) {
+        if (k == VT_GRAB_AT_U8 + 1) mid();
+        emit_word_four<kBE>(tc.W.w[k], tc.W.w[k + 1], q, carry4, KDC);
+      }
+      if (VT_GRAB_AT_U8 >= K8_WPT) mid();
       if (carry4) emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
     }
   } else {
+    mid();
     const Words tmp = tc.W;
     generic_chars(tmp, tc.lo, tc.lim, true, stage + off, kBE);
   }
@@ -494,9 +505,10 @@ struct Utf8Codec {
                                                unsigned& agg) {
     count_tile<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg);
   }
+  template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
-                                              unsigned off) {
-    emit_tile<kBE>(a, tc, reinterpret_cast<uint16_t*>(stage), off);
+                                              unsigned off, Mid&& mid) {
+    emit_tile<kBE>(a, tc, reinterpret_cast<uint16_t*>(stage), off, mid);
   }
 };
 

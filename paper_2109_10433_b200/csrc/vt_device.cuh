@@ -94,6 +94,19 @@ __device__ __forceinline__ unsigned long long load_status(unsigned long long* p)
   return a.load(cuda::memory_order_relaxed);
 }
 
+// Relaxed fetch-and-increment whose position among the (volatile) shared
+// stores of the emit is kept: the next-tile grab is issued part-way through
+// the decode and its round trip overlaps the rest of it.
+// (predicated inside the asm: a branch around it lets ptxas sink the block
+// behind the stores that follow)
+__device__ __forceinline__ void atom_inc_pinned(unsigned* p, bool pred, unsigned& r) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q atom.relaxed.gpu.global.add.u32 %0, [%1], 1;\n\t}"
+      : "+r"(r)
+      : "l"(p), "r"((unsigned)pred));
+}
+
 __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p) {
   cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
   return a.load(cuda::memory_order_relaxed);
