@@ -277,6 +277,18 @@ __device__ __noinline__ unsigned generic_chars(const Words& W, unsigned lo, unsi
   return q;
 }
 
+// Predicated 16-bit store at q, q += 2, when (~c | c2) has bit MASK set.
+template <uint32_t MASK>
+__device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t c2, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d;\n\t"
+      "lop3.or.b32 d|p, %1, %2, %3, 0x8A, 0;\n\t"  // (~a | b) & c
+      "@p st.shared.u16 [%0], %4;\n\t"
+      "@p add.u32 %0, %0, 2;\n\t}"
+      : "+r"(q)
+      : "r"(c), "r"(c2), "n"(MASK), "h"((unsigned short)v));
+}
+
 // Branch-free decode of one word: lead-attributed byte planes of each
 // character's UTF-16 unit (BMP only; words with 4-byte characters take
 // emit_word_four).  Predicated 16-bit stores at the running offset q.
@@ -285,7 +297,6 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
   const uint32_t c2 = c << 1;
-  const uint32_t lead7 = ~(c & ~c2) & H;               // lanes that start a character
   const uint32_t ge_e0 = c & c2 & (c << 2);            // bit 7: 3-byte (or 4-byte) lead
   // full-byte lane masks from bit 7 (PRMT sign-replicate selectors 8..B)
   const uint32_t mna = prmt(c, 0, 0xBA98);             // non-ASCII lanes
@@ -299,10 +310,12 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   // units of lanes 0,1 and 2,3 (little-endian; UTF-16BE swaps the two bytes)
   const uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140);
   const uint32_t u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
-  if (lead7 & 0x00000080u) { sts16(q, u01); q += 2; }
-  if (lead7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
-  if (lead7 & 0x00800000u) { sts16(q, u23); q += 2; }
-  if (lead7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
+  // lane i starts a character: (~c | c2) bit 8i+7, tested straight into the
+  // store predicate (one 3-input LOP3 per lane, no lead plane)
+  sts16_if_lead<0x00000080u>(q, c, c2, u01);
+  sts16_if_lead<0x00008000u>(q, c, c2, u01 >> 16);
+  sts16_if_lead<0x00800000u>(q, c, c2, u23);
+  sts16_if_lead<0x80000000u>(q, c, c2, u23 >> 16);
 }
 
 // Words with 4-byte characters: one unit per lane, like the BMP form.  A

@@ -40,6 +40,13 @@ __device__ __forceinline__ uint32_t op(uint32_t x, uint32_t k) {
   if (KIND == 14) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
                     asm volatile("mad.lo.u32 %0, %1, 16, %2;" : "=r"(r) : "r"(t), "r"(k)); }
   if (KIND == 15) { asm volatile("{.reg .u32 t; shl.b32 t, %1, 4; add.u32 %0, t, %2;}" : "=r"(r) : "r"(x), "r"(k)); }
+  // shr + add: ptxas fuses into LEA.HI; alone, and beside a LOP3
+  if (KIND == 16) { asm volatile("{.reg .u32 t; shr.u32 t, %1, 7; add.u32 %0, t, %2;}" : "=r"(r) : "r"(x), "r"(k)); }
+  if (KIND == 17) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .u32 u; shr.u32 u, %1, 7; add.u32 %0, u, %2;}" : "=r"(r) : "r"(t), "r"(k)); }
+  if (KIND == 18) asm volatile("{.reg .u32 t; shl.b32 t, %1, 8; add.u32 %0, t, %2;}" : "=r"(r) : "r"(x), "r"(k));
+  if (KIND == 19) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; selp.u32 %0, %1, %2, p;}" : "=r"(r) : "r"(t), "r"(k)); }
   return r;
 }
 
@@ -102,5 +109,9 @@ int main() {
   run<13>("setp+selp", 2);
   run<14>("LOP3+mad x16 imm", 2);
   run<15>("shl4+add (LEA?)", 2);
+  run<16>("shr7+add (LEA.HI)", 1);
+  run<17>("LOP3+LEA.HI", 2);
+  run<18>("shl8+add", 1);
+  run<19>("LOP3+setp+selp", 3);
   return 0;
 }
