@@ -162,8 +162,11 @@ __device__ __forceinline__ uint32_t special_lanes(uint32_t x, uint32_t l2, uint3
 // branch-free.  With the structure already checked, the only range errors are
 // on the lead and the byte after it (C0 C1; E0 + 80..9F; ED + A0..BF;
 // F0 + 80..8F; F4 + 90..BF; F5..FF): all lanes of a word at once.
-__device__ __noinline__ bool specials_fail(const Words W) {
-  uint32_t bad = 0;
+// Also counts the thread's 4-byte leads (F0..FF are special leads, so a
+// thread without special leads has none): bit 31 = range error, low byte =
+// 4-byte leads.  The count moved here off the hot loop (one ALU op per word).
+__device__ __noinline__ unsigned specials_check(const Words W) {
+  uint32_t bad = 0, cf = 0;
 #pragma unroll
   for (int k = 1; k <= K8_WPT; k++) {
     const uint32_t x = W.w[k], x2 = x << 1;
@@ -176,8 +179,9 @@ __device__ __noinline__ bool specials_fail(const Words W) {
     const uint32_t b5 = n1 << 2, b45 = (n1 | (n1 << 1)) << 2;  // bit 7: n1 >= A0 / >= 90
     bad |= (l2 & ~ge_c2) | (l3 & ~ge_e1 & ~b5) | (l3 & ge_ed & ~ge_ee & b5) |
            (l4 & ~ge_f1 & ~b45) | (l4 & ge_f4 & ~ge_f5 & b45) | (l4 & ge_f5);
+    cf += l4 >> 7;
   }
-  return (bad & H) != 0;
+  return ((bad & H) != 0 ? 0x80000000u : 0u) | ((cf * 0x01010101u) >> 24);
 }
 
 // Phase A over the 16 own words (SWAR, branch-free): structure check,
@@ -197,7 +201,7 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
     const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
     carry = (uint32_t)(need_plane(l2, l3, l4) >> 32);
   }
-  uint32_t viol = 0, spec = 0, ccont = 0, cfour = 0;
+  uint32_t viol = 0, spec = 0, ccont = 0;
 #pragma unroll
   for (int k = 1; k <= K8_WPT + 1; k++) {
     const uint32_t x = W.w[k], x2 = x << 1;
@@ -215,16 +219,17 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
       // (need_plane's IMAD.WIDE are quarter rate, and so is IMAD.HI, which
       // summed these before: 0.900 -> 0.883 ms cfg2, validation 0.335 -> 0.320)
       ccont += c >> 7;   // + continuation lanes
-      cfour += l4 >> 7;  // + 4-byte leads
     } else {
       viol |= (need ^ c) & 0x00808080u;  // next word: lanes that can blame our bytes
     }
   }
   ClassOut o;
-  const unsigned nc = (ccont * 0x01010101u) >> 24, n4 = (cfour * 0x01010101u) >> 24;
+  const unsigned nc = (ccont * 0x01010101u) >> 24;
+  const unsigned sc = (spec & H) != 0 ? specials_check(W) : 0u;
+  const unsigned n4 = sc & 0xFFu;
   o.chars = K8_BPT - nc;
   o.units = o.chars + n4;
-  o.viol = (viol & H) != 0 || ((spec & H) != 0 && specials_fail(W));
+  o.viol = (viol & H) != 0 || (sc >> 31) != 0;
   o.susp = (spec & H) != 0;
   o.four = n4 != 0;
   return o;
