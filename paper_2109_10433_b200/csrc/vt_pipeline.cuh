@@ -30,7 +30,7 @@ namespace vt {
 #define VT_GRAB_AT_U8 16
 #endif
 #ifndef VT_GRAB_AT_U16
-#define VT_GRAB_AT_U16 12
+#define VT_GRAB_AT_U16 10  // cfg3 A/B (r1n): 8 1.100, 9 1.087, 10 1.077, 11 1.082, 12 1.081 ms
 #endif
 
 #ifndef VT_COMPUTE_THREADS
