@@ -150,59 +150,120 @@ def cpu_reference_runner(kind):
 
 
 def host_input(cfg, size):
-    """The workload generated on the host (same generator as the device one)."""
-    import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
+    """The workload generated on the host by the test-side build of the same
+    generator header (oracle/lib/libvt_gen.so): the reference arm never loads
+    the product library."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import HostGen
 
-    import paper_2109_10433_b200 as vt
+    return HostGen().generate(cfg, size)[0]
 
-    chunks, total, c = [], 0, 0
-    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        while total < size:
-            for a in ex.map(lambda k: vt.generate_host_chunk(cfg, cfg, k)[0], range(c, c + 256)):
-                chunks.append(a)
-                total += len(a)
-                if total >= size:
+
+def cpu_info():
+    """nproc, CPU model and machine (an aarch64 host would run the
+    reference's emulated vector backend, proj/include/vtrans/vec128.hpp:7-10)."""
+    import platform
+
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
                     break
-            c += 256
-    host = np.concatenate(chunks)
-    n = _char_boundary(host, size, "u16" if cfg == 3 else "u8")
-    return np.ascontiguousarray(host[:n])
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model, "machine": platform.machine()}
+
+
+# bounded CPU sample per step for the round trip (4 GiB x 2 legs is minutes of CPU work)
+RT_CPU_SAMPLE = 512 << 20
+
+
+def cpu_reference_sample(cfg, host):
+    """The reference CPU path for config `cfg` on `host` (the config's whole
+    input; cfg5: a bounded prefix for the two-leg round trip).  Returns
+    (run(sample, threads) -> result, sample, kind, description, check(result))."""
+    import numpy as np
+
+    kind = CONFIGS[cfg][2]
+    if kind != "rt":
+        run, ck = cpu_reference_runner(kind)
+        return run, host, ck, f"whole cfg{cfg} input ({host.nbytes} bytes) per step", lambda r: None
+    m = _char_boundary(host, RT_CPU_SAMPLE, "u8")
+    sample = np.ascontiguousarray(host[:m])
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference
+
+    ck = "reference" if Reference.available() else "port"
+    impl = Reference() if ck == "reference" else Oracle()
+    out16 = np.empty(len(sample) + 8, dtype=np.uint16)
+    out8 = np.empty(3 * len(sample) + 16, dtype=np.uint8)
+
+    def run(h, t):
+        if ck == "reference":
+            _, r1 = impl.utf8_to_utf16(h, threads=t, out=out16)
+            o8, r2 = impl.utf16_to_utf8(out16[: r1.written], threads=t, out=out8)
+        else:
+            o16, r1 = impl.utf8_to_utf16(h, threads=t)
+            o8, r2 = impl.utf16_to_utf8(o16, threads=t)
+            out8[: len(o8)] = o8
+        return r2
+
+    def check(r):
+        assert r.error_at is None and r.written == sample.nbytes
+        assert np.array_equal(out8[: sample.nbytes], sample), "CPU round trip not byte-equal"
+    desc = (f"round trip 8->16->8 on the first {sample.nbytes} bytes of the cfg5 stream per step "
+            f"(bounded CPU sample), byte-equal checked")
+    return run, sample, ck, desc, check
 
 
 def run_reference_arm(args, rank):
-    """--impl reference: the reference's own CPU implementation on this box."""
+    """--impl reference: the reference's own CPU implementation on this box
+    (oracle/_ref: the unmodified library compiled out of tree; SIMD path on
+    character-boundary shards over all host threads), on the same workload,
+    config, metric and unit as the GPU arm.  Rank 0 only."""
     if rank != 0:
         return None
     desc, size, kind = CONFIGS[args.config]
-    if kind == "rt":
-        kind, size = "u8", 1 << 30  # the CPU round trip is timed on its first leg, 1 GiB
-    host = host_input(3 if kind == "u16" else args.config if args.config != 5 else 5, size)
+    host = host_input(args.config, size)
+    in_bytes = host.nbytes
     threads = os.cpu_count() or 1
-    run, ck = cpu_reference_runner(kind)
+    run, sample, ck, sample_desc, check = cpu_reference_sample(args.config, host)
     for _ in range(args.warmup):
-        run(host, threads)
+        r = run(sample, threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        r = run(host, threads)
+        r = run(sample, threads)
         times.append(time.perf_counter() - t0)
+    check(r)
     t = sum(times) / len(times)
-    in_bytes = host.nbytes
-    gbs = in_bytes / t / 1e9
-    return {
-        "metric": "input GB/s (validated UTF-8 -> UTF-16LE)" if kind == "u8" else "input GB/s (UTF-16LE -> UTF-8)",
-        "value": round(gbs, 4), "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": f"synthetic (seeded generator, BASELINE cfg{args.config} shape)",
-        "config": {"workload": desc, "input_bytes": in_bytes, "parallelism": f"cpu x{threads} threads"},
+    gbs = sample.nbytes / t / 1e9
+    line = {
+        "metric": METRICS[kind], "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u16" if kind == "u16" else "u8", "data": DATA,
+        "config": bench_config(args.config, in_bytes),
+        "parallelism": f"cpu x{threads} threads (character-boundary shards)",
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": ck,
-                         "sample": f"whole cfg{args.config} input ({in_bytes} bytes) per step, "
-                                   f"reference SIMD path on {threads} character-boundary shards"},
+                         "sample": sample_desc + f", reference SIMD path on {threads} character-boundary shards",
+                         **cpu_info()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result": {"consumed": r.consumed, "written": r.written, "error_at": r.error_at},
     }
+    return line
+
+
+METRICS = {"u8": "input GB/s (validated UTF-8 -> UTF-16LE)", "u16": "input GB/s (UTF-16LE -> UTF-8)",
+           "rt": "input GB/s (UTF-8 -> UTF-16LE -> UTF-8 round trip)"}
+DATA = "synthetic (seeded splitmix64 chunk generator, BASELINE cfg shape; corpora absent)"
+
+
+def bench_config(cfg, in_bytes):
+    """The workload-defining config dict, identical in both arms."""
+    return {"workload": CONFIGS[cfg][0], "input_bytes_per_gpu": int(in_bytes)}
 
 
 def timed_steps_flushed(step, steps, stream, flush, torch):
@@ -221,6 +282,107 @@ def timed_steps_flushed(step, steps, stream, flush, torch):
     return sum(a.elapsed_time(b) for a, b in evs)
 
 
+def combine_over_ranks(dist, device, res, n, in_bytes):
+    """The sharder's host combine across ranks (sharding.combine):
+    each rank holds one character-boundary shard of the job's stream; three
+    integers per rank are gathered (not data), the first failing shard decides
+    error_at and written, and the input bytes add up.  Works over NCCL
+    (device "cuda") or gloo (device "cpu", tests/test_bench_dist.py)."""
+    import numpy as np
+    import torch
+
+    from paper_2109_10433_b200 import TranscodeResult, sharding
+
+    world = dist.get_world_size()
+    mine = torch.tensor([res.consumed, res.written, -1 if res.error_at is None else res.error_at, n,
+                         in_bytes], dtype=torch.int64, device=device)
+    allr = [torch.zeros(5, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(allr, mine)
+    rows = [[int(v) for v in x.cpu().tolist()] for x in allr]
+    starts = np.concatenate([[0], np.cumsum([r[3] for r in rows])]).tolist()
+    rs = [TranscodeResult(r[0], r[1], None if r[2] < 0 else r[2]) for r in rows]
+    gres, _ = sharding.combine(starts, rs, starts[-1])
+    return gres, sum(r[4] for r in rows)
+
+
+def round_trip_weak(vt, torch, dist, rank, world, steps, peak):
+    """BASELINE cfg5 beside the headline line, at the same N: every rank holds
+    its own 4 GiB character-boundary shard of the cfg5 stream (disjoint chunk
+    ranges), converts UTF-8 -> UTF-16LE -> UTF-8 on its GPU and checks the result
+    equals its input byte for byte; per-rank results combine on the host
+    (combine_over_ranks).  Weak scaling: the shard size is fixed per GPU.
+    Device time with CUDA events, max over ranks."""
+    size = CONFIGS[5][1]
+    d_in, n, _ = vt.generate(5, size, chunk0=rank * 1_000_000)
+    d16 = torch.empty(n + 8, dtype=torch.int16, device="cuda")
+    r16 = vt.utf8_to_utf16_device(d_in, n, d16)
+    d8 = torch.empty(3 * r16.written + 16, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    ra = torch.zeros(3, dtype=torch.int64, device="cuda")
+    rb = torch.zeros(3, dtype=torch.int64, device="cuda")
+
+    def step():
+        vt.utf8_to_utf16_device(d_in, n, d16, stream=stream, d_res=ra)
+        vt.utf16_to_utf8_device(d16, r16.written, d8, stream=stream, d_res=rb)
+    for _ in range(3):
+        step()
+    k = max(3, min(steps, 10))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    r1, r2 = vt.result_from_device(ra), vt.result_from_device(rb)
+    equal = bool(r1.error_at is None and r2.error_at is None and r2.written == n
+                 and torch.equal(d8[:n], d_in[:n]))
+    ok = torch.tensor([1 if equal else 0], device="cuda")
+    gres, total_in = r2, n
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        gres, total_in = combine_over_ranks(dist, "cuda", r1, n, n)
+    out = {"workload": CONFIGS[5][0], "input_bytes_per_gpu": n, "utf16_units_per_gpu": r16.written,
+           "ms_per_step": round(ms, 4), "steps": k,
+           "value": round(total_in / (ms / 1e3) / 1e9, 2), "unit": "GB/s (aggregate UTF-8 input)",
+           "per_gpu_gbs": round(n / (ms / 1e3) / 1e9, 2),
+           "roofline_frac": round((2 * n + 4 * r16.written) / (ms / 1e3) / 1e9 / peak, 4),
+           "byte_equal_all_ranks": bool(ok.item()),
+           "combined_first_leg": {"consumed": gres.consumed, "written": gres.written,
+                                  "error_at": gres.error_at}}
+    del d_in, d16, d8
+    torch.cuda.empty_cache()
+    return out
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) without a launcher: one process per GPU under
+    torch.distributed.run on 127.0.0.1, as the driver launches it.  Fails
+    loudly when fewer than N GPUs are visible (the GPU arm only: the reference
+    arm runs on rank 0's host cores and the other ranks exit at once)."""
+    import socket
+
+    if args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} GPU(s) visible", file=sys.stderr)
+            return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -230,12 +392,17 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-rt", action="store_true", help="skip the cfg5 round-trip line beside cfg2")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         line = run_reference_arm(args, rank)
@@ -328,21 +495,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-        # combine the per-rank results (3 integers per rank; shards are independent)
-        from paper_2109_10433_b200 import TranscodeResult, sharding
-
-        mine = torch.tensor([res.consumed, res.written, -1 if res.error_at is None else res.error_at],
-                            device="cuda")
-        allr = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(world)]
-        dist.all_gather(allr, mine)
-        alln = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
-        dist.all_gather(alln, torch.tensor([n], device="cuda"))
-        starts = np.concatenate([[0], np.cumsum([int(x.item()) for x in alln])]).tolist()
-        rs = [TranscodeResult(int(x[0]), int(x[1]), None if int(x[2]) < 0 else int(x[2])) for x in allr]
-        gres, _ = sharding.combine(starts, rs, starts[-1])
-        tot = torch.tensor([in_bytes], device="cuda")
-        dist.all_reduce(tot)
-        total_in = int(tot.item())
+        gres, total_in = combine_over_ranks(dist, "cuda", res, n, in_bytes)
     else:
         gres = res
         total_in = in_bytes
@@ -364,11 +517,8 @@ def main():
     value = total_in / (per_step_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (ms / args.steps / 1e3) / 1e9
-    metric = ("input GB/s (UTF-16LE -> UTF-8)" if kind == "u16" else
-              "input GB/s (validated UTF-8 -> UTF-16LE)" if kind == "u8" else
-              "input GB/s (UTF-8 -> UTF-16LE -> UTF-8 round trip)")
     line = {
-        "metric": metric,
+        "metric": METRICS[kind],
         "value": round(value, 2),
         "unit": "GB/s",
         "n_gpus": world,
@@ -379,13 +529,15 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u16" if kind == "u16" else "u8",
-        "data": "synthetic (seeded splitmix64 chunk generator in HBM, BASELINE cfg shape; corpora absent)",
-        "config": {"workload": desc, "input_bytes_per_gpu": in_bytes, "output_elems_per_gpu": res.written,
-                   "chars_total": chars,
-                   "l2": ("input > 126 MB L2: no flush between steps" if flush is None
-                          else "L2 flushed (512 MiB write) between timed steps, each step timed "
-                               "by its own events (the bytes a call reads fit L2)"),
-                   "parallelism": f"shards x{world} (no collective)" if world > 1 else "single GPU"},
+        "data": DATA + ", generated in HBM",
+        "config": bench_config(args.config, in_bytes),
+        "output_elems_per_gpu": res.written,
+        "chars_total": chars,
+        "l2": ("input > 126 MB L2: no flush between steps" if flush is None
+               else "L2 flushed (512 MiB write) between timed steps, each step timed "
+                    "by its own events (the bytes a call reads fit L2)"),
+        "parallelism": f"{world} character-boundary shards, one per GPU (no collective)" if world > 1
+        else "single GPU",
         "gchars_per_s": round(chars / (per_step_ms / 1e3) / 1e9, 2),
         "result": {"consumed": gres.consumed, "written": gres.written, "error_at": gres.error_at},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -468,40 +620,64 @@ def main():
             b = torch.tensor([h2d, d2h], dtype=torch.int64, device="cuda")
             dist.all_reduce(b)
             h2d, d2h = int(b[0].item()), int(b[1].item())
+        # the same call on pageable buffers (a reference-style caller passing a
+        # std::vector): the library stages through its own pinned buffers
+        p_in = h_in.numpy().copy()
+        p_out = np.empty(h_out.numel() * h_out.element_size(), dtype=np.uint8)
+        fn(p_in.ctypes.data, n, p_out.ctypes.data, ctypes.byref(r))
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            rc = fn(p_in.ctypes.data, n, p_out.ctypes.data, ctypes.byref(r))
+            assert rc == 0, rc
+        dtp = (time.perf_counter() - t0) / k
+        if dist:
+            t = torch.tensor([dtp], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dtp = float(t.item())
         if rank == 0:
             line["e2e"] = {"value": round(total_in / dt / 1e9, 3), "unit": "GB/s",
                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                            "api": f"{fn.__name__} (drop-in boundary), pinned host buffers"
                                   + (f", {world} ranks, max over ranks" if world > 1 else ""),
-                           "ms_per_step": round(dt * 1e3, 3)}
+                           "ms_per_step": round(dt * 1e3, 3),
+                           "pageable": {"value": round(total_in / dtp / 1e9, 3), "unit": "GB/s",
+                                        "ms_per_step": round(dtp * 1e3, 3),
+                                        "api": f"{fn.__name__}, pageable (numpy) host buffers"}}
+
+    if args.config == 2 and not args.no_rt:
+        line["round_trip_cfg5"] = round_trip_weak(vt, torch, dist, rank, world, args.steps, peak)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ckind = "u16" if kind == "u16" else "u8"
         host = d_in[:n].cpu().numpy()
-        if ckind == "u16":
+        if kind == "u16":
             host = host.view(np.uint16)
         threads = os.cpu_count() or 1
-        run, ck = cpu_reference_runner(ckind)
+        run, sample, ck, sample_desc, check = cpu_reference_sample(args.config, host)
         best, cres = None, None
         for _ in range(3):
             t0 = time.perf_counter()
-            cres = run(host, threads)
+            cres = run(sample, threads)
             dt = time.perf_counter() - t0
             best = dt if best is None else min(best, dt)
+        check(cres)
         if kind != "rt":
             assert cres.written == res.written and cres.error_at == res.error_at, "CPU baseline disagrees"
-        # the reference's own design point: one thread, on a 64 MiB prefix
-        m = _char_boundary(host, (64 << 20) // host.itemsize, ckind)
-        t0 = time.perf_counter()
-        run(host[:m], 1)
-        t1 = time.perf_counter() - t0
+        single = ""
+        if kind != "rt":
+            # the reference's own design point: one thread, on a 64 MiB prefix
+            m = _char_boundary(sample, (64 << 20) // sample.itemsize, kind)
+            t0 = time.perf_counter()
+            run(sample[:m], 1)
+            single = round(m * sample.itemsize / (time.perf_counter() - t0) / 1e9, 3)
         line["cpu_baseline"] = {
-            "value": round(host.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": ck,
-            "sample": f"whole cfg{args.config} input ({host.nbytes} bytes{', first leg' if kind == 'rt' else ''}), "
-                      f"reference SIMD path (oracle/_ref, -O3 SSE4.1) on {threads} character-boundary "
-                      f"shards, best of 3; 1 thread on a {m * host.itemsize}-byte prefix: "
-                      f"{m * host.itemsize / t1 / 1e9:.3f} GB/s",
-            "single_thread_gbs": round(m * host.itemsize / t1 / 1e9, 3),
+            "value": round(sample.nbytes / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": ck,
+            "sample": f"{sample_desc}; reference SIMD path (oracle/_ref, -O3 SSE4.1) on {threads} "
+                      f"character-boundary shards, best of 3"
+                      + (f"; 1 thread on a 64 MiB prefix: {single} GB/s" if single else ""),
+            **({"single_thread_gbs": single} if single else {}),
+            **cpu_info(),
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -21,85 +21,27 @@
 //   validation.hpp:27,31   validate_utf8 / validate_utf16 GPU
 //   vec128.hpp:17-21       Backend, active_backend, ...   report the GPU backend
 //
-// The reference's scalar codec (vtrans::scalar::*) is NOT redefined here: it
-// stays the reference's (the oracle).  GPU code-point counts are in
-// vtrans::gpu.
+// The reference's scalar codec (vtrans::scalar::*) is declared (in
+// vtrans/codec_core.hpp) but NOT defined here: it stays the reference's (the
+// oracle).  GPU code-point counts are in vtrans::gpu.
 #pragma once
 
-#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <optional>
 #include <span>
-#include <vector>
+
+#include "vtrans/codec_core.hpp"
+#include "vtrans/utf16_to_utf8.hpp"
+#include "vtrans/utf8_to_utf16.hpp"
+#include "vtrans/validation.hpp"
+#include "vtrans/vec128.hpp"
 
 namespace vtrans {
-
-struct TranscodeResult {
-  std::size_t consumed = 0;             // input elements accepted
-  std::size_t written = 0;              // output elements produced
-  std::optional<std::size_t> error_at{};  // first invalid input index (then consumed == error_at)
-
-  bool ok() const { return !error_at.has_value(); }
-  friend bool operator==(const TranscodeResult&, const TranscodeResult&) = default;
-};
-
-struct PathCounters {
-  uint64_t total_bytes = 0;
-  uint64_t ascii64_blocks = 0;
-  uint64_t ascii64_bytes = 0;
-  uint64_t fast_ascii16 = 0;
-  uint64_t fast_twobyte16 = 0;
-  uint64_t fast_threebyte12 = 0;
-  uint64_t block12 = 0;
-  uint64_t scalar_fallback_chars = 0;
-  uint64_t inner_iterations = 0;
-};
-
-enum class Backend { emulated, native };
-
-// Backend reporting for link compatibility.  `native` is the GPU; there is no
-// second implementation to switch to, so force_emulated_backend only records
-// the request (active_backend() then reports `emulated` while the same GPU path
-// keeps running).
-Backend active_backend();
-void force_emulated_backend(bool force);
-bool native_backend_available();
-
-// UTF-8 -> UTF-16LE.  `out` must hold input.size() units.  `validate` is
-// accepted for signature compatibility; the GPU always validates (allowed: the
-// reference leaves non-validating results on invalid input unspecified).
-TranscodeResult utf8_to_utf16(std::span<const uint8_t> input, uint16_t* out, bool validate,
-                              PathCounters* counters = nullptr);
-std::vector<uint16_t> utf8_to_utf16(std::span<const uint8_t> input, bool validate,
-                                    TranscodeResult& res, PathCounters* counters = nullptr);
-
-// UTF-16LE -> UTF-8.  `out` must hold 3 * input.size() + 16 bytes.
-TranscodeResult utf16_to_utf8(std::span<const uint16_t> input, uint8_t* out);
-std::vector<uint8_t> utf16_to_utf8(std::span<const uint16_t> input, TranscodeResult& res);
-
-// Streaming UTF-8 validator over 64-byte blocks, same layout and member
-// meaning as the reference's: `error` is all zero while the stream is valid,
-// `prev_incomplete` all zero when no sequence is left dangling at the end
-// (here: its bytes, then their count at [4]), `prev_input` the last 16 bytes.
-struct Utf8BlockValidator {
-  std::array<uint8_t, 16> error{};
-  std::array<uint8_t, 16> prev_input{};
-  std::array<uint8_t, 16> prev_incomplete{};
-
-  void feed(const uint8_t* block64);
-  bool ok_so_far() const;
-  bool finish() const;
-};
-
-bool validate_utf8(std::span<const uint8_t> bytes);
-std::optional<std::size_t> validate_utf16(std::span<const uint16_t> units);
-
 namespace gpu {
 // Code points, or nullopt when invalid (same meaning as the reference's
 // scalar::count_codepoints_utf8/16, proj/include/vtrans/codec_core.hpp:66-67).
 std::optional<std::size_t> count_codepoints_utf8(std::span<const uint8_t> bytes);
 std::optional<std::size_t> count_codepoints_utf16(std::span<const uint16_t> units);
 }  // namespace gpu
-
 }  // namespace vtrans

@@ -23,6 +23,10 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libvtrans_gpu.so")
+# A/B tooling (tools/ab_*.sh) points VT_LIB at an experimental build of the same
+# library instead of overwriting the in-tree product .so.
+if os.environ.get("VT_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["VT_LIB"])
 
 __all__ = [
     "TranscodeResult", "VtransError", "lib", "utf8_to_utf16", "utf16_to_utf8", "validate_utf8",

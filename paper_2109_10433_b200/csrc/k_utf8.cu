@@ -288,10 +288,15 @@ __device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t 
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 d;\n\t"
       "lop3.or.b32 d|p, %1, %2, %3, 0x8A, 0;\n\t"  // (~a | b) & c
-      "@p st.shared.u16 [%0], %4;\n\t"
+#ifdef VT_EXP_PREDOFF
+      "{\n\t.reg .pred p2;\n\tsetp.eq.and.u32 p2, %5, 0xFFFFFFFF, p;\n\t"
+      "@p2 st.shared.u16 [%5], %4;\n\t}\n\t"
+#elif !defined(VT_EXP_NOSTS)
+      "@p st.shared.u16 [%5], %4;\n\t"
+#endif
       "@p add.u32 %0, %0, 2;\n\t}"
       : "+r"(q)
-      : "r"(c), "r"(c2), "n"(MASK), "h"((unsigned short)v));
+      : "r"(c), "r"(c2), "n"(MASK), "h"((unsigned short)v), "r"(VT_LANE_ADDR(q)));
 }
 
 // Branch-free decode of one word: lead-attributed byte planes of each

@@ -43,16 +43,37 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+// A/B probes of the staging-store cost (timing only, output is garbage):
+// VT_EXP_LANESTS keeps every store but sends lane i to bank i (no conflicts).
+#ifdef VT_EXP_LANESTS
+#define VT_LANE_ADDR(a) (((a) & ~0x7Fu) | ((threadIdx.x & 31u) << 2) | ((a) & 3u))
+#elif defined(VT_EXP_PREDOFF)
+// VT_EXP_PREDOFF: every store's address and value are computed, the store is
+// predicated off at run time (measures the emit's ALU work without the stores)
+#define VT_LANE_ADDR(a) ((a) | 0xFFFF0000u)
+#else
+#define VT_LANE_ADDR(a) (a)
+#endif
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  a = VT_LANE_ADDR(a);
 #ifdef VT_EXP_NOSTS
   asm volatile("" ::"r"(a), "r"(v));
+#elif defined(VT_EXP_PREDOFF)
+  if (a == 0xFFFFFFFFu) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 #else
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 #endif
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
   // stores the low byte of v (no masking instruction needed)
+  a = VT_LANE_ADDR(a);
+#ifdef VT_EXP_NOSTS
+  asm volatile("" ::"r"(a), "r"(v));
+#elif defined(VT_EXP_PREDOFF)
+  if (a == 0xFFFFFFFFu) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+#else
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+#endif
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;

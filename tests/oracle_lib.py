@@ -21,6 +21,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE_SO = os.path.join(ROOT, "oracle", "lib", "libvt_oracle.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "libvtrans_ref.so")
+GEN_SO = os.path.join(ROOT, "oracle", "lib", "libvt_gen.so")
 
 
 class CRes(C.Structure):
@@ -53,7 +54,7 @@ def _p16(a):
 
 
 def ensure_built() -> None:
-    if not os.path.exists(ORACLE_SO):
+    if not (os.path.exists(ORACLE_SO) and os.path.exists(GEN_SO)):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=True)
 
 
@@ -238,3 +239,35 @@ class Reference:
         k = self._exh(_p8(out))
         assert k == len(out)
         return out
+
+
+class HostGen:
+    """The synthetic BASELINE workloads generated on the host from the same
+    header as the device generator (oracle/gen_host.cpp -> libvt_gen.so), so
+    bench.py's reference arm never loads the product library."""
+
+    def __init__(self):
+        ensure_built()
+        L = _Lib(GEN_SO, "vtg_")
+        self._draws = L.fn("chunk_draws", C.c_uint64, C.c_int)
+        self._chunk = L.fn("host_chunk", C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p,
+                           C.c_uint64, C.POINTER(C.c_uint64))
+        self._gen = L.fn("generate", C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_int,
+                         C.POINTER(C.c_uint64))
+
+    def chunk(self, cfg: int, seed: int, chunk: int):
+        cap = int(self._draws(cfg)) * 64 + 64
+        out = np.empty(cap, dtype=np.uint16 if cfg == 3 else np.uint8)
+        fb = C.c_uint64()
+        k = int(self._chunk(cfg, seed, chunk, out.ctypes.data, cap, C.byref(fb)))
+        return out[:k], (None if fb.value == 0xFFFFFFFFFFFFFFFF else int(fb.value))
+
+    def generate(self, cfg: int, size: int, seed: int | None = None, threads: int | None = None):
+        """(array, first_injected): the first `size` elements of the stream cut
+        after the last whole character, exactly what the device generator
+        (paper_2109_10433_b200.generate) writes for chunk0 = 0."""
+        seed = cfg if seed is None else seed
+        out = np.empty(size + 16, dtype=np.uint16 if cfg == 3 else np.uint8)
+        fb = C.c_uint64()
+        n = int(self._gen(cfg, seed, size, out.ctypes.data, threads or os.cpu_count() or 1, C.byref(fb)))
+        return out[:n], (None if fb.value == 0xFFFFFFFFFFFFFFFF else int(fb.value))

@@ -47,6 +47,38 @@ __device__ __forceinline__ uint32_t op(uint32_t x, uint32_t k) {
   if (KIND == 18) asm volatile("{.reg .u32 t; shl.b32 t, %1, 8; add.u32 %0, t, %2;}" : "=r"(r) : "r"(x), "r"(k));
   if (KIND == 19) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
                     asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; selp.u32 %0, %1, %2, p;}" : "=r"(r) : "r"(t), "r"(k)); }
+  if (KIND == 20) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .u32 u; add.u32 u, %1, %2; add.u32 %0, u, %1;}" : "=r"(r) : "r"(t), "r"(k)); }  // LOP3 + IADD3?
+  if (KIND == 21) { asm volatile("{.reg .u32 u; add.u32 u, %1, %2; add.u32 %0, u, %1;}" : "=r"(r) : "r"(x), "r"(k)); }  // IADD3 alone
+  if (KIND == 22) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .pred p; setp.ne.u32 p, %2, 0; selp.u32 %0, %1, %2, p;}" : "=r"(r) : "r"(t), "r"(k)); }  // LOP3 + SEL (fixed pred)
+  if (KIND == 23) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .pred p; setp.lt.u32 p, %1, %2; @p add.u32 %0, %1, 7; @!p add.u32 %0, %1, 9;}" : "=r"(r) : "r"(t), "r"(k)); }  // LOP3 + ISETP + 2 pred add
+  if (KIND == 24) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("mul.hi.u32 %0, %1, 0x4000000;" : "=r"(r) : "r"(t)); }  // LOP3 + IMAD.HI as shift
+  if (KIND == 25) { uint32_t t, u; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("lop3.b32 %0, %1, %2, %1, 0x6a;" : "=r"(u) : "r"(t), "r"(k));
+                    asm volatile("mul.hi.u32 %0, %1, 0x4000000;" : "=r"(r) : "r"(u)); }  // 2 LOP3 + 1 IMAD.HI
+  if (KIND == 26) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("mul.lo.u32 %0, %1, 64;" : "=r"(r) : "r"(t)); }  // LOP3 + IMAD.SHL
+  if (KIND == 27) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("add.u32 %0, %1, 0x1234;" : "=r"(r) : "r"(t)); }  // LOP3 + VIADD (imm)
+  if (KIND == 28) { asm volatile("add.u32 %0, %1, 0x1234;" : "=r"(r) : "r"(x)); }  // VIADD alone
+  if (KIND == 29) { uint32_t t; asm volatile("prmt.b32 %0, %1, %2, 0x5140;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("mad.lo.u32 %0, %1, %2, %1;" : "=r"(r) : "r"(t), "r"(k)); }  // PRMT + IMAD
+  if (KIND == 30) { uint32_t t; asm volatile("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("mad.lo.u32 %0, %1, %2, %1;" : "=r"(r) : "r"(t), "r"(k)); }  // SHF + IMAD
+  if (KIND == 31) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .pred p; setp.lt.u32 p, %1, %2; selp.u32 %0, 5, 9, p;}" : "=r"(r) : "r"(t), "r"(k)); }  // LOP3 + ISETP + SEL
+  if (KIND == 32) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("fma.rn.f32 %0, %1, %1, %1;" : "=f"(*(float*)&r) : "f"(__uint_as_float(t))); }  // LOP3 + FFMA
+  if (KIND == 33) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("{.reg .b64 w; mad.wide.u32 w, %1, %2, 0; cvt.u32.u64 %0, w;}" : "=r"(r) : "r"(t), "r"(k)); }  // LOP3 + IMAD.WIDE
+  if (KIND == 34) { uint32_t t; asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("bfe.u32 %0, %1, 6, 6;" : "=r"(r) : "r"(t)); }  // LOP3 + BFE (what SASS?)
+  if (KIND == 35) { uint32_t t, u; asm volatile("mad.lo.u32 %0, %1, %2, %1;" : "=r"(t) : "r"(x), "r"(k));
+                    asm volatile("mad.lo.u32 %0, %1, %2, %1;" : "=r"(u) : "r"(t), "r"(k));
+                    asm volatile("lop3.b32 %0, %1, %2, %1, 0x96;" : "=r"(r) : "r"(u), "r"(k)); }  // 2 IMAD + LOP3
   return r;
 }
 
@@ -113,5 +145,21 @@ int main() {
   run<17>("LOP3+LEA.HI", 2);
   run<18>("shl8+add", 1);
   run<19>("LOP3+setp+selp", 3);
+  run<20>("LOP3+IADD3", 2);
+  run<21>("IADD3 alone", 1);
+  run<22>("LOP3+SEL", 2);
+  run<23>("LOP3+ISETP+2 pred add", 4);
+  run<24>("LOP3+IMAD.HI shift", 2);
+  run<25>("2 LOP3+IMAD.HI", 3);
+  run<26>("LOP3+IMAD.SHL", 2);
+  run<27>("LOP3+VIADD", 2);
+  run<28>("VIADD alone", 1);
+  run<29>("PRMT+IMAD", 2);
+  run<30>("SHF+IMAD", 2);
+  run<31>("LOP3+ISETP+SEL", 3);
+  run<32>("LOP3+FFMA", 2);
+  run<33>("LOP3+IMAD.WIDE", 2);
+  run<34>("LOP3+BFE", 2);
+  run<35>("2 IMAD+LOP3", 3);
   return 0;
 }
