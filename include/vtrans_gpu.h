@@ -79,6 +79,17 @@ int vt_host_validate_utf16(const uint16_t* in, uint64_t n, int64_t* first_err);
 int vt_host_count_utf8(const uint8_t* in, uint64_t n, int64_t* count);
 int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count);
 
+/* ---- non-validating UTF-8 -> UTF-16LE --------------
+ * The reference's validate=false path (proj/src/utf8_to_utf16.cpp:230-239,
+ * vtrans::utf8_to_utf16(..., validate=false)): no structure or range checks.
+ * Identical results on valid input; on invalid input the output is
+ * unspecified (as in the reference) but never exceeds n units, and the result
+ * reports no error (consumed = n). */
+int vt_utf8_to_utf16_nonvalidating_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out,
+                                         vt_result* d_res, vt_stream stream);
+int vt_host_utf8_to_utf16_nonvalidating(const uint8_t* in, uint64_t n, uint16_t* out,
+                                        vt_result* res);
+
 /* ---- UTF-16 big-endian and byte-order marks --------
  * The reference converts big-endian UTF-16 with a separate byte-swap pass
  * around its little-endian kernels (proj/src/harness.cpp:178-199); here the
@@ -160,6 +171,18 @@ int vt_host_utf8_class_counts(const uint8_t* in, uint64_t n, uint64_t counts[4],
  * [d_offsets[i], d_offsets[i+1]).  Writes the first error index or -1. */
 int vt_validate_utf8_batch(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t count,
                            int64_t* d_first_err, vt_stream stream);
+/* Batched transcoding, one launch for the whole batch (the reference's fuzz
+ * driver makes one call per case, proj/src/harness.cpp:357-375).  String i is
+ * [d_offsets[i], d_offsets[i+1]) of d_data; its output is written at the same
+ * offset in d_out (UTF-8 -> UTF-16: in units, capacity = the string's byte
+ * length) or at 3 * d_offsets[i] bytes (UTF-16 -> UTF-8: capacity 3 bytes per
+ * unit); d_res[i] is its result, exactly as one vt_host_* call on that string
+ * would return it.  validate = 0 selects the non-validating decode (same
+ * result on valid strings). */
+int vt_utf8_to_utf16_batch(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           uint16_t* d_out, vt_result* d_res, int validate, vt_stream stream);
+int vt_utf16_to_utf8_batch(const uint16_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           uint8_t* d_out, vt_result* d_res, vt_stream stream);
 /* Verdict (1 = valid) of every 1-, 2- and 3-byte input in the enumeration
  * order of acceptance C3 (proj/tests/acceptance.cpp:147-167);
  * d_verdicts holds 16843008 bytes. */
@@ -168,13 +191,28 @@ int vt_exhaustive_short_verdicts(uint8_t* d_verdicts, vt_stream stream);
 /* ---- multi-GPU sharder ------------------------------------------------------
  * Splits a host buffer at character boundaries into `ndev` shards (0 = one
  * per visible GPU; shard k runs on GPU k % count),
- * runs the single-GPU path per shard concurrently (one host thread per GPU,
- * no collective), and combines: output offsets by exclusive scan of the
+ * runs the single-GPU path per shard concurrently (one persistent host worker
+ * thread per GPU, no collective), and combines: output offsets by exclusive scan of the
  * per-shard `written`, error from the first failing shard. */
 int vt_sharded_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, int ndev,
                              vt_result* res);
 int vt_sharded_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, int ndev,
                              vt_result* res);
+/* Device-resident shards (weak scaling without PCIe): shard k is
+ * d_in[k][0..n[k]) on device dev[k], and the shards are consecutive
+ * character-boundary pieces of one stream (cut with vt_split_point_*).  Every
+ * device transcodes its own shard into d_out[k] (capacity as for the single
+ * calls) concurrently on a library-owned stream; no host threads, no copies,
+ * no collective.  shard_res[k] (may be NULL) = shard k's own result,
+ * out_offsets[k] (may be NULL) = where shard k's output goes in the combined
+ * stream, *res = the combined result (first failing shard decides).  Several
+ * shards may name the same device (they run in order on it). */
+int vt_sharded_device_utf8_to_utf16(int nshards, const int* dev, const uint8_t* const* d_in,
+                                    const uint64_t* n, uint16_t* const* d_out,
+                                    vt_result* shard_res, uint64_t* out_offsets, vt_result* res);
+int vt_sharded_device_utf16_to_utf8(int nshards, const int* dev, const uint16_t* const* d_in,
+                                    const uint64_t* n, uint8_t* const* d_out,
+                                    vt_result* shard_res, uint64_t* out_offsets, vt_result* res);
 /* Host-side split-point rules the sharder uses (exposed for tests). */
 uint64_t vt_split_point_utf8(const uint8_t* in, uint64_t n, uint64_t cut);
 uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut);

@@ -329,3 +329,82 @@ uint64_t vto_exhaustive_short_verdicts(uint8_t* verdict) {
       }
   return k;
 }
+
+/* ---- batched transcoding (the checker for vt_*_batch) ----------------------
+ * String i = [offsets[i], offsets[i+1]); output at the same offset (UTF-16
+ * units) or 3 * offsets[i] (UTF-8 bytes); one result per string.  The scalar
+ * codec per string, as the reference's fuzz driver calls it per case
+ * (proj/src/harness.cpp:357-375). */
+void vto_utf8_to_utf16_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                             uint16_t* out, vto_result* res) {
+  for (uint64_t i = 0; i < count; i++)
+    vto_utf8_to_utf16(data + offsets[i], offsets[i + 1] - offsets[i], out + offsets[i], res + i);
+}
+
+void vto_utf16_to_utf8_batch(const uint16_t* data, const uint64_t* offsets, uint64_t count,
+                             uint8_t* out, vto_result* res) {
+  for (uint64_t i = 0; i < count; i++)
+    vto_utf16_to_utf8(data + offsets[i], offsets[i + 1] - offsets[i], out + 3 * offsets[i], res + i);
+}
+
+/* Differential-fuzz cases shaped like the reference's run_fuzz
+ * (proj/src/harness.cpp:388-436, its gen_valid_utf8 at :330-350): case i of
+ * kind i % 3 -- 0: random bytes, 1: valid UTF-8 drawn from one of six
+ * class mixes, 2: the same with one bit flipped; lengths uniform in
+ * [0, max_len].  Our own splitmix64 stream (not the reference's mt19937), so
+ * the cases have the reference's shape, not its exact bytes.  Writes
+ * offsets[0..count] and the packed bytes; returns the total, or UINT64_MAX if
+ * it would exceed `cap`. */
+static uint64_t fz_next(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint32_t fz_scalar(uint64_t* s, int cls) {
+  switch (cls) {
+    case 0: return (uint32_t)(fz_next(s) % 0x80);
+    case 1: return 0x80 + (uint32_t)(fz_next(s) % (0x800 - 0x80));
+    case 2: {
+      uint32_t cp;
+      do cp = 0x800 + (uint32_t)(fz_next(s) % (0x10000 - 0x800));
+      while (cp >= 0xD800 && cp <= 0xDFFF);
+      return cp;
+    }
+    default: return 0x10000 + (uint32_t)(fz_next(s) % (0x110000 - 0x10000));
+  }
+}
+
+uint64_t vto_fuzz_cases(uint64_t seed, uint64_t count, uint32_t max_len, uint8_t* data,
+                        uint64_t* offsets, uint64_t cap) {
+  static const int mixes[6][4] = {{100, 0, 0, 0}, {22, 78, 0, 0}, {1, 0, 99, 0},
+                                  {0, 0, 0, 100}, {25, 25, 25, 25}, {50, 0, 50, 0}};
+  uint64_t st = seed, pos = 0;
+  offsets[0] = 0;
+  for (uint64_t i = 0; i < count; i++) {
+    const int kind = (int)(i % 3);
+    const uint64_t target = max_len ? fz_next(&st) % ((uint64_t)max_len + 1) : 0;
+    if (pos + target + 4 > cap) return UINT64_MAX;
+    const uint64_t start = pos;
+    if (kind == 0) {
+      for (uint64_t k = 0; k < target; k++) data[pos++] = (uint8_t)fz_next(&st);
+    } else {
+      const int* mix = mixes[fz_next(&st) % 6];
+      while (pos - start < target) {
+        int roll = (int)(fz_next(&st) % 100), cls = 0;
+        for (int k = 0; k < 4; k++) {
+          if (roll < mix[k]) {
+            cls = k;
+            break;
+          }
+          roll -= mix[k];
+        }
+        pos += vto_encode_utf8(fz_scalar(&st, cls), data + pos);
+      }
+      if (kind == 2 && pos > start) data[start + fz_next(&st) % (pos - start)] ^= (uint8_t)(1u << (fz_next(&st) % 8));
+    }
+    offsets[i + 1] = pos;
+  }
+  return pos;
+}

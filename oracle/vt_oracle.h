@@ -35,6 +35,12 @@ void vto_utf16_to_utf8_mt(const uint16_t* s, uint64_t n, uint8_t* out, int threa
 void vto_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
                              int64_t* first_err);
 uint64_t vto_exhaustive_short_verdicts(uint8_t* verdict);
+void vto_utf8_to_utf16_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                             uint16_t* out, vto_result* res);
+void vto_utf16_to_utf8_batch(const uint16_t* data, const uint64_t* offsets, uint64_t count,
+                             uint8_t* out, vto_result* res);
+uint64_t vto_fuzz_cases(uint64_t seed, uint64_t count, uint32_t max_len, uint8_t* data,
+                        uint64_t* offsets, uint64_t cap);
 
 #ifdef __cplusplus
 }

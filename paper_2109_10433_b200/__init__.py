@@ -33,6 +33,8 @@ __all__ = [
     "validate_utf16", "count_utf8", "count_utf16", "utf8_to_utf16_device", "utf16_to_utf8_device",
     "validate_utf8_device", "validate_utf16_device", "validate_utf8_batch",
     "exhaustive_short_verdicts", "sharded_utf8_to_utf16", "sharded_utf16_to_utf8",
+    "sharded_device_utf8_to_utf16", "sharded_device_utf16_to_utf8", "utf8_to_utf16_batch_device",
+    "utf16_to_utf8_batch_device", "utf8_to_utf16_nonvalidating", "utf8_to_utf16_nonvalidating_device",
     "split_point_utf8", "split_point_utf16", "generate", "launch_count", "device_count",
 ]
 
@@ -107,8 +109,16 @@ def lib():
                                               C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                               C.POINTER(C.c_int64)]),
         "vt_exhaustive_short_verdicts": (C.c_int, [_vp, _vp]),
+        "vt_utf8_to_utf16_batch": (C.c_int, [_vp, _vp, C.c_uint64, _vp, _vp, C.c_int, _vp]),
+        "vt_utf16_to_utf8_batch": (C.c_int, [_vp, _vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_utf8_to_utf16_nonvalidating_async": (C.c_int, [_vp, C.c_uint64, _vp, _vp, _vp]),
+        "vt_host_utf8_to_utf16_nonvalidating": (C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_CRes)]),
         "vt_sharded_utf8_to_utf16": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
         "vt_sharded_utf16_to_utf8": (C.c_int, [_vp, C.c_uint64, _vp, C.c_int, C.POINTER(_CRes)]),
+        "vt_sharded_device_utf8_to_utf16": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                      C.POINTER(_CRes)]),
+        "vt_sharded_device_utf16_to_utf8": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                      C.POINTER(_CRes)]),
         "vt_split_point_utf8": (C.c_uint64, [_vp, C.c_uint64, C.c_uint64]),
         "vt_split_point_utf16": (C.c_uint64, [_vp, C.c_uint64, C.c_uint64]),
         "vt_gen_sizes": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp]),
@@ -381,6 +391,46 @@ def validate_utf8_batch(d_data, d_offsets, count: int, d_first_err, stream=None)
            "validate_utf8_batch")
 
 
+def utf8_to_utf16_batch_device(d_data, d_offsets, count: int, d_out, d_res, validate: bool = True,
+                               stream=None) -> None:
+    """vt_utf8_to_utf16_batch: string i = d_data[d_offsets[i]:d_offsets[i+1]],
+    its units at d_out[d_offsets[i]:], its result in d_res[i] (int64 x3)."""
+    _check(lib().vt_utf8_to_utf16_batch(d_data.data_ptr(), d_offsets.data_ptr(), count, d_out.data_ptr(),
+                                        d_res.data_ptr(), int(bool(validate)), _stream_ptr(stream)),
+           "utf8_to_utf16_batch")
+
+
+def utf16_to_utf8_batch_device(d_units, d_offsets, count: int, d_out, d_res, stream=None) -> None:
+    """vt_utf16_to_utf8_batch: string i's bytes at d_out[3 * d_offsets[i]:]."""
+    _check(lib().vt_utf16_to_utf8_batch(d_units.data_ptr(), d_offsets.data_ptr(), count, d_out.data_ptr(),
+                                        d_res.data_ptr(), _stream_ptr(stream)), "utf16_to_utf8_batch")
+
+
+def utf8_to_utf16_nonvalidating(data) -> tuple[np.ndarray, TranscodeResult]:
+    """The reference's validate=false path (vt_host_utf8_to_utf16_nonvalidating):
+    identical to utf8_to_utf16 on valid input; unspecified output otherwise."""
+    a = _bytes_view(data)
+    out = np.empty(len(a) + 8, dtype=np.uint16)
+    r = _CRes()
+    _check(lib().vt_host_utf8_to_utf16_nonvalidating(_ptr(a), len(a), out.ctypes.data, C.byref(r)),
+           "utf8_to_utf16_nonvalidating")
+    res = TranscodeResult._of(r)
+    return out[: res.written], res
+
+
+def utf8_to_utf16_nonvalidating_device(d_in, n: int, d_out, stream=None, d_res=None):
+    if d_res is not None:
+        _check(lib().vt_utf8_to_utf16_nonvalidating_async(d_in.data_ptr(), n, d_out.data_ptr(),
+                                                          d_res.data_ptr(), _stream_ptr(stream)),
+               "utf8_to_utf16_nonvalidating_async")
+        return None
+    import torch
+
+    res = torch.zeros(3, dtype=torch.int64, device=d_in.device)
+    utf8_to_utf16_nonvalidating_device(d_in, n, d_out, stream, res)
+    return result_from_device(res)
+
+
 def exhaustive_short_verdicts(device="cuda"):
     import torch
 
@@ -410,6 +460,33 @@ def sharded_utf16_to_utf8(units, ndev: int = 0):
            "sharded_utf16_to_utf8")
     res = TranscodeResult._of(r)
     return out[: res.written], res
+
+
+def _sharded_device(fn, what, shards, outs):
+    """shards: [(tensor, n)] consecutive character-boundary pieces of one stream,
+    each on its own device (tensor.device); outs: output tensors, one per shard."""
+    k = len(shards)
+    devs = (C.c_int * k)(*[t.device.index for t, _ in shards])
+    ins = (C.c_void_p * k)(*[t.data_ptr() for t, _ in shards])
+    ns = (C.c_uint64 * k)(*[n for _, n in shards])
+    os_ = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    per = (_CRes * k)()
+    offs = (C.c_uint64 * k)()
+    r = _CRes()
+    _check(fn(k, devs, ins, ns, os_, per, offs, C.byref(r)), what)
+    return TranscodeResult._of(r), [TranscodeResult._of(x) for x in per], [int(x) for x in offs]
+
+
+def sharded_device_utf8_to_utf16(shards, outs):
+    """Device-resident shards (vt_sharded_device_utf8_to_utf16): returns
+    (combined result, per-shard results, per-shard output offsets)."""
+    return _sharded_device(lib().vt_sharded_device_utf8_to_utf16, "sharded_device_utf8_to_utf16",
+                           shards, outs)
+
+
+def sharded_device_utf16_to_utf8(shards, outs):
+    return _sharded_device(lib().vt_sharded_device_utf16_to_utf8, "sharded_device_utf16_to_utf8",
+                           shards, outs)
 
 
 def split_point_utf8(data, cut: int) -> int:

@@ -52,6 +52,124 @@ __global__ void batch_validate_kernel(const uint8_t* data, const uint64_t* offse
   first_err[i] = first_error_seq(data + s, e - s);
 }
 
+// ---- batched transcoding (one thread per string) ------------------------------
+// The reference's fuzz and exhaustive drivers transcode millions of short
+// strings one call at a time (proj/src/harness.cpp:357-375, 388-436); here a
+// whole batch is one launch.  String i = data[off[i], off[i+1]); its output
+// goes to the same offsets in units (UTF-8 -> UTF-16: capacity = its byte
+// length) or to 3*off[i] in bytes (UTF-16 -> UTF-8: capacity 3 per unit), so
+// no scan is needed; res[i] = its TranscodeResult.  The decode follows
+// proj/src/codec_core.cpp:5-125 character by character, stopping at the first
+// invalid one (validate), or without checks (validate = 0: the reference's
+// validate=false, same result on valid input, bounded output otherwise).
+__global__ void batch_u8to16_kernel(const uint8_t* data, const uint64_t* off, uint64_t count,
+                                    uint16_t* out, vt_result* res, int validate) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  const uint64_t b = off[s], n = off[s + 1] - b;
+  const uint8_t* p = data + b;
+  uint16_t* o = out + b;
+  uint64_t i = 0, q = 0;
+  long long err = -1;
+  while (i < n) {
+    const unsigned b0 = p[i];
+    if (b0 < 0x80u) {
+      o[q++] = (uint16_t)b0;
+      i++;
+      continue;
+    }
+    unsigned len = (b0 & 0xE0u) == 0xC0u ? 2u : (b0 & 0xF0u) == 0xE0u ? 3u : (b0 & 0xF8u) == 0xF0u ? 4u : 0u;
+    if (validate) {
+      if (len == 0 || first_error_seq(p + i, min((uint64_t)len, n - i)) == 0 || i + len > n) {
+        err = (long long)i;
+        break;
+      }
+    } else {
+      // no checks: a malformed lead or a cut sequence decodes as far as the
+      // input goes (each unit still consumes at least one byte)
+      if (len == 0) len = 1;
+      if (i + len > n) len = (unsigned)(n - i);
+    }
+    uint32_t cp = len == 1 ? b0 : b0 & (0x7Fu >> len);
+    for (unsigned k = 1; k < len; k++) cp = (cp << 6) | (p[i + k] & 0x3Fu);
+    if (cp >= 0x10000u && len == 4) {
+      cp -= 0x10000u;
+      o[q++] = (uint16_t)(0xD800u + (cp >> 10));
+      o[q++] = (uint16_t)(0xDC00u + (cp & 0x3FFu));
+    } else {
+      o[q++] = (uint16_t)cp;
+    }
+    i += len;
+  }
+  vt_result r;
+  r.written = q;
+  r.consumed = err < 0 ? n : (uint64_t)err;
+  r.error_at = err;
+  res[s] = r;
+}
+
+__global__ void batch_u16to8_kernel(const uint16_t* data, const uint64_t* off, uint64_t count,
+                                    uint8_t* out, vt_result* res) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  const uint64_t b = off[s], n = off[s + 1] - b;
+  const uint16_t* p = data + b;
+  uint8_t* o = out + 3 * b;
+  uint64_t i = 0, q = 0;
+  long long err = -1;
+  while (i < n) {
+    uint32_t cp = p[i];
+    unsigned len = 1;
+    if ((cp & 0xF800u) == 0xD800u) {  // surrogate: a high one followed by a low one
+      if (cp >= 0xDC00u || i + 1 >= n || (p[i + 1] & 0xFC00u) != 0xDC00u) {
+        err = (long long)i;
+        break;
+      }
+      cp = 0x10000u + ((cp - 0xD800u) << 10) + (p[i + 1] - 0xDC00u);
+      len = 2;
+    }
+    if (cp < 0x80u) {
+      o[q++] = (uint8_t)cp;
+    } else if (cp < 0x800u) {
+      o[q++] = (uint8_t)(0xC0u | (cp >> 6));
+      o[q++] = (uint8_t)(0x80u | (cp & 0x3Fu));
+    } else if (cp < 0x10000u) {
+      o[q++] = (uint8_t)(0xE0u | (cp >> 12));
+      o[q++] = (uint8_t)(0x80u | ((cp >> 6) & 0x3Fu));
+      o[q++] = (uint8_t)(0x80u | (cp & 0x3Fu));
+    } else {
+      o[q++] = (uint8_t)(0xF0u | (cp >> 18));
+      o[q++] = (uint8_t)(0x80u | ((cp >> 12) & 0x3Fu));
+      o[q++] = (uint8_t)(0x80u | ((cp >> 6) & 0x3Fu));
+      o[q++] = (uint8_t)(0x80u | (cp & 0x3Fu));
+    }
+    i += len;
+  }
+  vt_result r;
+  r.written = q;
+  r.consumed = err < 0 ? n : (uint64_t)err;
+  r.error_at = err;
+  res[s] = r;
+}
+
+int launch_utf8_to_utf16_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                               uint16_t* out, vt_result* res, int validate, cudaStream_t s) {
+  if (count == 0) return 0;
+  const unsigned threads = 128;
+  batch_u8to16_kernel<<<(unsigned)((count + threads - 1) / threads), threads, 0, s>>>(
+      data, offsets, count, out, res, validate);
+  return (int)cudaGetLastError();
+}
+
+int launch_utf16_to_utf8_batch(const uint16_t* data, const uint64_t* offsets, uint64_t count,
+                               uint8_t* out, vt_result* res, cudaStream_t s) {
+  if (count == 0) return 0;
+  const unsigned threads = 128;
+  batch_u16to8_kernel<<<(unsigned)((count + threads - 1) / threads), threads, 0, s>>>(
+      data, offsets, count, out, res);
+  return (int)cudaGetLastError();
+}
+
 // Input number k of the 1/2/3-byte enumeration (acceptance.cpp:147-167).
 __global__ void exhaustive_short_kernel(uint8_t* verdicts) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;

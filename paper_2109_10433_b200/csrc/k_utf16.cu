@@ -281,7 +281,11 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
     // (end tiles: the zeros outside the input counted as one ASCII unit each)
     tc.cnt = (kTranscode ? c.bytes : c.chars) - (K16_UPT - (hi - tc.lo));
     unsigned total;
+#if VT_SCAN1
+    off = block_excl_scan1<NT, Sync>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), scan, total);
+#else
     off = block_excl_scan<NT, Sync, false>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), scan, total);
+#endif
     if ((total >> kErrShift) == 0) {
       tc.simple = true;
       agg = total;

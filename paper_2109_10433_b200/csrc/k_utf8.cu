@@ -235,6 +235,35 @@ __device__ __forceinline__ ClassOut classify(const Words& W) {
   return o;
 }
 
+// Non-validating count (the reference's validate=false path, proj/src/
+// utf8_to_utf16.cpp:230-239): no structure or range checks, only what the
+// emit will store -- one unit per non-continuation byte, plus the low
+// surrogate of every F0..FF lead whose next byte is a continuation (that
+// lane is where emit_word_four<kNV=true> stores it).  Bounded by the input
+// length on any input: each extra unit consumes a continuation byte.
+__device__ __forceinline__ ClassOut classify_nv(const Words& W) {
+  uint32_t ccont = 0, pairs = 0, four = 0;
+#pragma unroll
+  for (int k = 1; k <= K8_WPT; k++) {
+    const uint32_t x = W.w[k], x2 = x << 1;
+    const uint32_t c = x & ~x2 & H;                       // continuation lanes
+    const uint32_t f4 = x & x2 & (x << 2) & (x << 3) & H;  // F0..FF lanes
+    const uint32_t n = W.w[k + 1];
+    // continuation plane of the byte after each lane
+    const uint32_t cn = prmt(c, n & ~(n << 1) & H, 0x4321);
+    ccont += c >> 7;
+    pairs += (f4 & cn) >> 7;
+    four |= f4;
+  }
+  ClassOut o;
+  o.chars = K8_BPT - ((ccont * 0x01010101u) >> 24);
+  o.units = o.chars + ((pairs * 0x01010101u) >> 24);
+  o.viol = false;
+  o.susp = false;
+  o.four = four != 0;
+  return o;
+}
+
 // ---- generic path (ends of the input, tiles with an error): rare, per byte --
 // Counts (units or characters) of the characters starting at positions
 // [lo, lim) of the thread's bytes; with `dst`, also writes their units.
@@ -299,6 +328,33 @@ __device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t 
       : "r"(c), "r"(c2), "n"(MASK), "h"((unsigned short)v), "r"(VT_LANE_ADDR(q)));
 }
 
+// The four predicated stores of one word in one asm block (the running
+// address stays in one register; the high units move down inside).
+#ifndef VT_STS4
+#define VT_STS4 0
+#endif
+__device__ __forceinline__ void sts16x4_if_lead(uint32_t& q, uint32_t c, uint32_t c2, uint32_t u01,
+                                                uint32_t u23) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, p2, p3;\n\t.reg .b32 d0, d1, d2, d3, h1, h3;\n\t"
+      "lop3.or.b32 d0|p0, %1, %2, 0x00000080, 0x8A, 0;\n\t"
+      "lop3.or.b32 d1|p1, %1, %2, 0x00008000, 0x8A, 0;\n\t"
+      "lop3.or.b32 d2|p2, %1, %2, 0x00800000, 0x8A, 0;\n\t"
+      "lop3.or.b32 d3|p3, %1, %2, 0x80000000, 0x8A, 0;\n\t"
+      "shr.b32 h1, %3, 16;\n\t"
+      "shr.b32 h3, %4, 16;\n\t"
+      "@p0 st.shared.b16 [%0], %3;\n\t"
+      "@p0 add.u32 %0, %0, 2;\n\t"
+      "@p1 st.shared.b16 [%0], h1;\n\t"
+      "@p1 add.u32 %0, %0, 2;\n\t"
+      "@p2 st.shared.b16 [%0], %4;\n\t"
+      "@p2 add.u32 %0, %0, 2;\n\t"
+      "@p3 st.shared.b16 [%0], h3;\n\t"
+      "@p3 add.u32 %0, %0, 2;\n\t}"
+      : "+r"(q)
+      : "r"(c), "r"(c2), "r"(u01), "r"(u23));
+}
+
 // Branch-free decode of one word: lead-attributed byte planes of each
 // character's UTF-16 unit (BMP only; words with 4-byte characters take
 // emit_word_four).  Predicated 16-bit stores at the running offset q.
@@ -322,10 +378,14 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
   // lane i starts a character: (~c | c2) bit 8i+7, tested straight into the
   // store predicate (one 3-input LOP3 per lane, no lead plane)
+#if VT_STS4
+  sts16x4_if_lead(q, c, c2, u01, u23);
+#else
   sts16_if_lead<0x00000080u>(q, c, c2, u01);
   sts16_if_lead<0x00008000u>(q, c, c2, u01 >> 16);
   sts16_if_lead<0x00800000u>(q, c, c2, u23);
   sts16_if_lead<0x80000000u>(q, c, c2, u23 >> 16);
+#endif
 }
 
 // Words with 4-byte characters: one unit per lane, like the BMP form.  A
@@ -337,7 +397,7 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
 // stores per word, not 8).  `carry4` (bit 7) says the previous word's lane 3
 // was a 4-byte lead of this thread; a lead in the thread's last byte has its
 // ls lane in the next thread and is finished by emit_tail_ls.
-template <bool kBE>
+template <bool kBE, bool kNV = false>
 __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t& q,
                                                uint32_t& carry4, uint32_t KDC) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
@@ -371,7 +431,9 @@ __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t&
   }
   u01 = lop3<0xCA>(prmt(m4, 0, 0x1100), hs01, u01);
   u23 = lop3<0xCA>(prmt(m4, 0, 0x3322), hs23, u23);
-  const uint32_t st7 = lead7 | ls7;
+  // (non-validating: an ls lane stores only if it is a continuation, so the
+  // stores match classify_nv's count on any input)
+  const uint32_t st7 = kNV ? lead7 | (ls7 & c & ~c2) : lead7 | ls7;
   if (st7 & 0x00000080u) { sts16(q, u01); q += 2; }
   if (st7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
   if (st7 & 0x00800000u) { sts16(q, u23); q += 2; }
@@ -397,7 +459,7 @@ struct TileCount {
   unsigned cnt;      // units (transcode) or characters of the thread
 };
 
-template <bool kTranscode, int NT, class Sync>
+template <bool kTranscode, int NT, class Sync, bool kNV = false>
 __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsigned* red,
                                            unsigned* scan, TileCount& tc, unsigned& off,
                                            unsigned& agg) {
@@ -426,7 +488,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
   tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
   const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
-  const ClassOut co = classify(tc.W);
+  const ClassOut co = kNV ? classify_nv(tc.W) : classify(tc.W);
 #ifdef VT_PHASES
   {
     const long long t = clock64() + (co.units == 0x7FFFFFFF ? 1 : 0);
@@ -449,7 +511,11 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     // (end tiles: the zeros outside the input counted as one ASCII character each)
     tc.cnt = (kTranscode ? co.units : co.chars) - (K8_BPT - (hi - tc.lo));
     unsigned total;
+#if VT_SCAN1
+    off = block_excl_scan1<NT, Sync>(my_err == kNone ? tc.cnt : (1u << kErrShift), scan, total);
+#else
     off = block_excl_scan<NT, Sync, false>(my_err == kNone ? tc.cnt : (1u << kErrShift), scan, total);
+#endif
     if ((total >> kErrShift) == 0) {
       tc.simple = true;
       agg = total;
@@ -475,7 +541,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
 }
 
 // ---- per-tile back half: decode into the staging buffer -----------------------
-template <bool kBE, class Mid>
+template <bool kBE, bool kNV, class Mid>
 __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
                                           unsigned off, Mid&& mid) {
   if (tc.simple) {
@@ -498,10 +564,12 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
 #pragma unroll
       for (int k = 1; k <= K8_WPT; k++) {
         if (k == VT_GRAB_AT_U8 + 1) mid();
-        emit_word_four<kBE>(tc.W.w[k], tc.W.w[k + 1], q, carry4, KDC);
+        emit_word_four<kBE, kNV>(tc.W.w[k], tc.W.w[k + 1], q, carry4, KDC);
       }
       if (VT_GRAB_AT_U8 >= K8_WPT) mid();
-      if (carry4) emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
+      // (non-validating: only if the byte after the lead is a continuation)
+      if (carry4 && (!kNV || (tc.W.w[K8_WPT + 1] & 0xC0u) == 0x80u))
+        emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
     }
   } else {
     mid();
@@ -514,7 +582,7 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
 #define VT_NSTAGE8 1
 #endif
 
-template <bool kBE>
+template <bool kBE, bool kNV = false>
 struct Utf8Codec {
   using Args = U8Args;
   using TileCount = vt::TileCount;
@@ -526,12 +594,12 @@ struct Utf8Codec {
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
                                                unsigned& agg) {
-    count_tile<kTranscode, NT, Sync>(a, tile, red, scan, tc, off, agg);
+    count_tile<kTranscode, NT, Sync, kNV>(a, tile, red, scan, tc, off, agg);
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
                                               unsigned off, Mid&& mid) {
-    emit_tile<kBE>(a, tc, reinterpret_cast<uint16_t*>(stage), off, mid);
+    emit_tile<kBE, kNV>(a, tc, reinterpret_cast<uint16_t*>(stage), off, mid);
   }
 };
 
@@ -665,17 +733,20 @@ unsigned rows_utf8(unsigned long long head, unsigned long long n) {
 #define VT_K8_MINB 4
 #endif
 // UTF-8 -> UTF-16LE (kBE = false) or UTF-16BE (kBE = true)
-template <bool kBE>
+// (kNV: the non-validating variant, LE output only)
+template <bool kBE, bool kNV = false>
 __global__ void __launch_bounds__(kPipeBlock, VT_K8_MINB) utf8_transcode_kernel(U8Args a) {
   extern __shared__ __align__(16) uint8_t k8_dyn_smem[];
-  transcode_body<Utf8Codec<kBE>>(a, *reinterpret_cast<PipeSmem<Utf8Codec<kBE>>*>(k8_dyn_smem));
+  transcode_body<Utf8Codec<kBE, kNV>>(
+      a, *reinterpret_cast<PipeSmem<Utf8Codec<kBE, kNV>>*>(k8_dyn_smem));
 }
 
 static int set_smem_attr() {
   // (no carveout preference: forcing the largest shared-memory carveout
   // leaves too little L1 for the input loads -- measured 1.37 vs 1.32 ms on
   // cfg3)
-  for (const void* f : {(const void*)utf8_transcode_kernel<false>, (const void*)utf8_transcode_kernel<true>}) {
+  for (const void* f : {(const void*)utf8_transcode_kernel<false>, (const void*)utf8_transcode_kernel<true>,
+                        (const void*)utf8_transcode_kernel<false, true>}) {
     const int rc = (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sizeof(PipeSmem<Utf8Codec<false>>));
     if (rc) return rc;
@@ -690,6 +761,9 @@ int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s) {
     utf8_transcode_kernel<false><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<false>>), s>>>(a);
   else if (mode == kModeTranscodeBE)
     utf8_transcode_kernel<true><<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<true>>), s>>>(a);
+  else if (mode == kModeTranscodeNV)
+    utf8_transcode_kernel<false, true>
+        <<<grid, kPipeBlock, sizeof(PipeSmem<Utf8Codec<false, true>>), s>>>(a);
   else if (mode == kModeLength)
     utf8_validate_rows_kernel<true><<<grid, 256, 0, s>>>(a);
   else

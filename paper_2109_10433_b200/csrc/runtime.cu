@@ -8,7 +8,10 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdio>
+#include <deque>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -122,17 +125,69 @@ int ensure_rows(Scratch& sc, cudaStream_t s, size_t rows) {
   return 0;
 }
 
+// Scratch is keyed by the stream's unique id (cudaStreamGetId), not its handle:
+// the special handles (legacy default stream, cudaStreamPerThread) name a
+// different real stream in every host thread, and two threads on
+// cudaStreamPerThread must not share a control block while their kernels run
+// concurrently.  Ids are never reused, so entries of destroyed streams are
+// evicted once the table grows past kScratchMax: an entry nobody holds (use
+// count 1) is freed after a device synchronize (its last kernels may still be
+// in flight on the dead stream).
+constexpr size_t kScratchMax = 64;
 std::mutex g_scratch_mu;
-std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Scratch>> g_scratch;
+std::map<std::pair<int, unsigned long long>, std::shared_ptr<Scratch>> g_scratch;
 
-Scratch* scratch_for(int dev, cudaStream_t s) {
-  std::lock_guard<std::mutex> lk(g_scratch_mu);
-  auto& p = g_scratch[{dev, s}];
-  if (!p) {
-    p.reset(new Scratch());
-    p->dev = dev;
+void free_scratch(Scratch& sc) {
+  if (sc.ctl) cudaFree(sc.ctl);
+  if (sc.status) cudaFree(sc.status);
+  if (sc.d_res) cudaFree(sc.d_res);
+  if (sc.h_res) cudaFreeHost(sc.h_res);
+  if (sc.rows) cudaFree(sc.rows);
+  sc.ctl = nullptr;
+  sc.status = nullptr;
+  sc.d_res = nullptr;
+  sc.h_res = nullptr;
+  sc.rows = nullptr;
+}
+
+// (caller holds g_scratch_mu; `keep` is the entry being handed out)
+void evict_idle_scratch(const Scratch* keep) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+    if (it->second.get() != keep && it->second.use_count() == 1) {
+      cudaSetDevice(it->second->dev);
+      cudaDeviceSynchronize();
+      free_scratch(*it->second);
+      it = g_scratch.erase(it);
+    } else {
+      ++it;
+    }
   }
-  return p.get();
+  if (cur >= 0) cudaSetDevice(cur);
+}
+
+int scratch_for(int dev, cudaStream_t s, std::shared_ptr<Scratch>& out) {
+  unsigned long long id = 0;
+  VT_TRY(cudaStreamGetId(s, &id));
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  auto& p = g_scratch[{dev, id}];
+  if (!p) {
+    p = std::make_shared<Scratch>();
+    p->dev = dev;
+    if (g_scratch.size() > kScratchMax) evict_idle_scratch(p.get());
+  }
+  out = p;
+  return 0;
+}
+
+// The kernels' control blocks carry host-side state (the status epoch, grown
+// arrays), so a call cannot be recorded into a CUDA graph: every replay would
+// reuse one epoch and read stale tile prefixes.  Capture is refused.
+int refuse_capture(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  VT_TRY(cudaStreamIsCapturing(s, &st));
+  return st == cudaStreamCaptureStatusNone ? 0 : VT_E_ARG;
 }
 
 // Ensures capacity for `tiles` status words and returns the epoch to use.
@@ -174,7 +229,8 @@ int grid_for(unsigned tiles, int occ, int sms) {
 int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint64_t n,
                     uint16_t* d_out, vt_result* d_res, cudaStream_t s, int mode,
                     const unsigned* d_skip = nullptr) {
-  const bool transcode = mode == vt::kModeTranscode || mode == vt::kModeTranscodeBE;
+  const bool transcode = mode == vt::kModeTranscode || mode == vt::kModeTranscodeBE ||
+                         mode == vt::kModeTranscodeNV;
   if (!d_res || (n && !d_in) || (transcode && n && !d_out)) return VT_E_ARG;
   vt::U8Args a;
   const uintptr_t p = (uintptr_t)d_in;
@@ -232,7 +288,8 @@ int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, ui
 }
 
 struct Target {
-  Scratch* sc;
+  std::shared_ptr<Scratch> hold;  // keeps the entry alive while in use
+  Scratch* sc = nullptr;
   DeviceInfo di;
 };
 
@@ -240,7 +297,9 @@ int target(cudaStream_t s, Target& t) {
   int dev;
   VT_TRY(current_device(dev));
   VT_TRY(device_info(dev, t.di));
-  t.sc = scratch_for(dev, s);
+  VT_TRY(refuse_capture(s));
+  VT_TRY(scratch_for(dev, s, t.hold));
+  t.sc = t.hold.get();
   return 0;
 }
 
@@ -448,27 +507,34 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
     VT_TRY(cudaEventRecord(c->pev[b], s));
     return 0;
   };
-  for (size_t k = 0; k < K && k < (size_t)HostCtx::kPipeBufs; k++) VT_TRY(issue(k));
+  // Every exit below drains all pipeline streams first: no copy may still read
+  // the caller's input or write the caller's output after the call returns.
+  int rc = 0;
+  for (size_t k = 0; k < K && k < (size_t)HostCtx::kPipeBufs && rc == 0; k++) rc = issue(k);
   uint64_t written = 0;
   res->error_at = -1;
   res->consumed = n;
-  int rc = 0;
-  for (size_t k = 0; k < K; k++) {
+  for (size_t k = 0; k < K && rc == 0; k++) {
     const int b = (int)(k % HostCtx::kPipeBufs);
-    VT_TRY(cudaEventSynchronize(c->pev[b]));
+    rc = (int)cudaEventSynchronize(c->pev[b]);
+    if (rc) break;
     const vt_result r = c->ph_res[b];
-    if (written + r.written > out_cap_elems) return VT_E_ARG;
+    if (written + r.written > out_cap_elems) {
+      rc = VT_E_ARG;
+      break;
+    }
     t_d2h += r.written * sizeof(Out);
     if (r.written) {
       if (pin_out) {
-        VT_TRY(cudaMemcpyAsync(out + written, c->pd_out[b], r.written * sizeof(Out),
-                               cudaMemcpyDeviceToHost, c->ps[b]));
+        rc = (int)cudaMemcpyAsync(out + written, c->pd_out[b], r.written * sizeof(Out),
+                                  cudaMemcpyDeviceToHost, c->ps[b]);
       } else {
-        VT_TRY(cudaMemcpyAsync(c->ph_out[b], c->pd_out[b], r.written * sizeof(Out),
-                               cudaMemcpyDeviceToHost, c->ps[b]));
-        VT_TRY(cudaStreamSynchronize(c->ps[b]));
-        std::memcpy(out + written, c->ph_out[b], r.written * sizeof(Out));
+        rc = (int)cudaMemcpyAsync(c->ph_out[b], c->pd_out[b], r.written * sizeof(Out),
+                                  cudaMemcpyDeviceToHost, c->ps[b]);
+        if (!rc) rc = (int)cudaStreamSynchronize(c->ps[b]);
+        if (!rc) std::memcpy(out + written, c->ph_out[b], r.written * sizeof(Out));
       }
+      if (rc) break;
     }
     written += r.written;
     if (r.error_at >= 0) {
@@ -476,12 +542,12 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
       res->consumed = (uint64_t)res->error_at;
       break;
     }
-    if (k + HostCtx::kPipeBufs < K) {
-      rc = issue(k + HostCtx::kPipeBufs);
-      if (rc) break;
-    }
+    if (k + HostCtx::kPipeBufs < K) rc = issue(k + HostCtx::kPipeBufs);
   }
-  for (int i = 0; i < HostCtx::kPipeBufs; i++) VT_TRY(cudaStreamSynchronize(c->ps[i]));
+  for (int i = 0; i < HostCtx::kPipeBufs; i++) {
+    const int r2 = (int)cudaStreamSynchronize(c->ps[i]);
+    if (!rc) rc = r2;
+  }
   res->written = written;
   return rc;
 }
@@ -704,6 +770,19 @@ int vt_host_count_utf16(const uint16_t* in, uint64_t n, int64_t* count) {
   return 0;
 }
 
+int vt_utf8_to_utf16_nonvalidating_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out,
+                                         vt_result* d_res, vt_stream stream) {
+  return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscodeNV);
+}
+
+int vt_host_utf8_to_utf16_nonvalidating(const uint8_t* in, uint64_t n, uint16_t* out,
+                                        vt_result* res) {
+  return host_transcode(in, n, out, n, res,
+                        [](const uint8_t* i, uint64_t k, uint16_t* o, vt_result* r, cudaStream_t s) {
+                          return run_utf8(i, k, o, r, s, vt::kModeTranscodeNV);
+                        });
+}
+
 int vt_utf8_to_utf16be_async(const uint8_t* d_in, uint64_t n, uint16_t* d_out, vt_result* d_res,
                              vt_stream stream) {
   return run_utf8(d_in, n, d_out, d_res, (cudaStream_t)stream, vt::kModeTranscodeBE);
@@ -892,6 +971,26 @@ int vt_validate_utf8_batch(const uint8_t* d_data, const uint64_t* d_offsets, uin
                                         (cudaStream_t)stream);
 }
 
+int vt_utf8_to_utf16_batch(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           uint16_t* d_out, vt_result* d_res, int validate, vt_stream stream) {
+  if (count && (!d_data || !d_offsets || !d_out || !d_res)) return VT_E_ARG;
+  int dev;
+  VT_TRY(current_device(dev));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_utf8_to_utf16_batch(d_data, d_offsets, count, d_out, d_res, validate,
+                                        (cudaStream_t)stream);
+}
+
+int vt_utf16_to_utf8_batch(const uint16_t* d_data, const uint64_t* d_offsets, uint64_t count,
+                           uint8_t* d_out, vt_result* d_res, vt_stream stream) {
+  if (count && (!d_data || !d_offsets || !d_out || !d_res)) return VT_E_ARG;
+  int dev;
+  VT_TRY(current_device(dev));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return vt::launch_utf16_to_utf8_batch(d_data, d_offsets, count, d_out, d_res,
+                                        (cudaStream_t)stream);
+}
+
 int vt_exhaustive_short_verdicts(uint8_t* d_verdicts, vt_stream stream) {
   int dev;
   VT_TRY(current_device(dev));
@@ -921,6 +1020,101 @@ uint64_t vt_split_point_utf16(const uint16_t* in, uint64_t n, uint64_t cut) {
 
 namespace {
 
+// One persistent host thread per device for the host-pointer sharder.  A
+// shard's host context (stream, pinned staging, device buffers) belongs to the
+// thread that runs it (thread_local HostCtx), so per-call threads would build
+// and abandon one per shard per call; these workers keep theirs for the life
+// of the process.  The pool is never destroyed (workers idle on a condition
+// variable at exit).
+class DeviceWorkers {
+ public:
+  static DeviceWorkers& get() {
+    static DeviceWorkers* w = new DeviceWorkers();
+    return *w;
+  }
+  // Runs fn on device dev's worker; the returned job is waited with wait().
+  struct Job {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool done = false;
+    std::function<void()> fn;
+  };
+  void submit(int dev, const std::shared_ptr<Job>& job) {
+    Worker& w = worker(dev);
+    {
+      std::lock_guard<std::mutex> lk(w.mu);
+      w.q.push_back(job);
+    }
+    w.cv.notify_one();
+  }
+  static void wait(const std::shared_ptr<Job>& job) {
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [&] { return job->done; });
+  }
+
+ private:
+  struct Worker {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::shared_ptr<Job>> q;
+    std::thread th;
+  };
+  std::mutex mu_;
+  std::map<int, std::unique_ptr<Worker>> ws_;
+
+  Worker& worker(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto& w = ws_[dev];
+    if (!w) {
+      w.reset(new Worker());
+      Worker* wp = w.get();
+      wp->th = std::thread([wp, dev] {
+        cudaSetDevice(dev);
+        for (;;) {
+          std::shared_ptr<Job> job;
+          {
+            std::unique_lock<std::mutex> lk(wp->mu);
+            wp->cv.wait(lk, [&] { return !wp->q.empty(); });
+            job = wp->q.front();
+            wp->q.pop_front();
+          }
+          job->fn();
+          {
+            std::lock_guard<std::mutex> lk(job->mu);
+            job->done = true;
+          }
+          job->cv.notify_all();
+        }
+      });
+      wp->th.detach();
+    }
+    return *w;
+  }
+};
+
+// Combines per-shard results of consecutive character-boundary shards
+// (SURVEY.md 8(a) D/E): output offsets by exclusive scan of `written`, the
+// first failing shard decides error_at; shards after it hold no part of the
+// defined output.
+void combine_shards(const std::vector<uint64_t>& st, const vt_result* rs, int k_n,
+                    uint64_t* offsets, vt_result* res) {
+  uint64_t written = 0;
+  res->error_at = -1;
+  res->consumed = st[k_n];
+  bool stopped = false;
+  for (int k = 0; k < k_n; k++) {
+    if (offsets) offsets[k] = written;
+    if (stopped) continue;
+    written += rs[k].written;
+    if (rs[k].error_at >= 0) {
+      res->error_at = (int64_t)st[k] + rs[k].error_at;
+      res->consumed = (uint64_t)res->error_at;
+      stopped = true;
+    }
+  }
+  res->written = written;
+}
+
 template <class In, class Out, class Split, class One>
 int sharded(const In* in, uint64_t n, Out* out, int ndev, uint64_t mult, vt_result* res,
             Split split, One one) {
@@ -930,41 +1124,91 @@ int sharded(const In* in, uint64_t n, Out* out, int ndev, uint64_t mult, vt_resu
     cudaGetLastError();
     return VT_E_NODEVICE;
   }
-  // ndev shards; shard k runs on device k % avail (more shards than devices
-  // share a device, each on its own host thread and stream)
+  // ndev shards; shard k runs on device k % avail (shards sharing a device run
+  // one after the other on its worker)
   if (ndev <= 0) ndev = avail;
   std::vector<uint64_t> st(ndev + 1, 0);
   for (int k = 1; k < ndev; k++) st[k] = std::max(st[k - 1], split(in, n, n / ndev * k));
   st[ndev] = n;
   std::vector<vt_result> rs(ndev);
   std::vector<int> rcs(ndev, 0);
-  std::vector<std::thread> ts;
+  std::vector<std::shared_ptr<DeviceWorkers::Job>> jobs;
   for (int k = 0; k < ndev; k++) {
-    ts.emplace_back([&, k] {
-      rcs[k] = (int)cudaSetDevice(k % avail);
-      if (rcs[k]) return;
-      // shard k's output fits in [mult*st[k], mult*st[k+1]) of the caller's buffer
-      rcs[k] = one(in + st[k], st[k + 1] - st[k], out + mult * st[k], &rs[k]);
-    });
+    auto job = std::make_shared<DeviceWorkers::Job>();
+    // shard k's output fits in [mult*st[k], mult*st[k+1]) of the caller's buffer
+    job->fn = [&, k] { rcs[k] = one(in + st[k], st[k + 1] - st[k], out + mult * st[k], &rs[k]); };
+    DeviceWorkers::get().submit(k % avail, job);
+    jobs.push_back(job);
   }
-  for (auto& t : ts) t.join();
+  for (auto& j : jobs) DeviceWorkers::wait(j);
   for (int k = 0; k < ndev; k++)
     if (rcs[k]) return rcs[k];
-  // combine: exclusive scan of written, first failing shard decides
-  uint64_t written = 0;
-  res->error_at = -1;
-  res->consumed = n;
-  for (int k = 0; k < ndev; k++) {
-    if (written != mult * st[k] && rs[k].written)
-      std::memmove(out + written, out + mult * st[k], rs[k].written * sizeof(Out));
-    written += rs[k].written;
-    if (rs[k].error_at >= 0) {
-      res->error_at = (int64_t)st[k] + rs[k].error_at;
-      res->consumed = (uint64_t)res->error_at;
-      break;
+  std::vector<uint64_t> off(ndev);
+  combine_shards(st, rs.data(), ndev, off.data(), res);
+  // compact the shards' outputs (in order: a move may overwrite the tail of an
+  // earlier shard's source only after that shard moved)
+  for (int k = 0; k < ndev && off[k] < res->written; k++)
+    if (off[k] != mult * st[k] && rs[k].written)
+      std::memmove(out + off[k], out + mult * st[k], rs[k].written * sizeof(Out));
+  return 0;
+}
+
+// Device-resident shards: per device one library-owned stream and result
+// slots; the calling thread enqueues every shard, then waits for all.
+struct ShardDev {
+  cudaStream_t s = nullptr;
+  vt_result* d_res = nullptr;
+  vt_result* h_res = nullptr;
+  int cap = 0;
+};
+std::mutex g_shard_mu;
+std::map<int, ShardDev> g_shard_dev;
+
+template <class In, class Out, class Async>
+int sharded_device(int nshards, const int* dev, const In* const* d_in, const uint64_t* n,
+                   Out* const* d_out, vt_result* shard_res, uint64_t* out_offsets, vt_result* res,
+                   Async async) {
+  if (nshards <= 0 || !dev || !d_in || !n || !d_out || !res) return VT_E_ARG;
+  int cur;
+  VT_TRY(current_device(cur));
+  std::lock_guard<std::mutex> lk(g_shard_mu);
+  std::map<int, int> used;  // result slots per device
+  std::vector<int> slot(nshards);
+  int rc = 0;
+  for (int k = 0; k < nshards && !rc; k++) {
+    slot[k] = used[dev[k]]++;
+    rc = (int)cudaSetDevice(dev[k]);
+    if (rc) break;
+    ShardDev& sd = g_shard_dev[dev[k]];
+    if (!sd.s) rc = (int)cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    if (!rc && sd.cap < nshards) {
+      // (all earlier users of this device's slots were waited for)
+      if (sd.d_res) cudaFree(sd.d_res);
+      if (sd.h_res) cudaFreeHost(sd.h_res);
+      rc = (int)cudaMalloc(&sd.d_res, nshards * sizeof(vt_result));
+      if (!rc) rc = (int)cudaMallocHost(&sd.h_res, nshards * sizeof(vt_result));
+      sd.cap = rc ? 0 : nshards;
     }
+    if (!rc) rc = async(d_in[k], n[k], d_out[k], sd.d_res + slot[k], (vt_stream)sd.s);
+    if (!rc)
+      rc = (int)cudaMemcpyAsync(sd.h_res + slot[k], sd.d_res + slot[k], sizeof(vt_result),
+                                cudaMemcpyDeviceToHost, sd.s);
   }
-  res->written = written;
+  for (auto& u : used) {  // wait for every device that got work
+    cudaSetDevice(u.first);
+    const int r2 = (int)cudaStreamSynchronize(g_shard_dev[u.first].s);
+    if (!rc) rc = r2;
+  }
+  cudaSetDevice(cur);
+  if (rc) return rc;
+  std::vector<uint64_t> st(nshards + 1, 0);
+  std::vector<vt_result> rs(nshards);
+  for (int k = 0; k < nshards; k++) {
+    rs[k] = g_shard_dev[dev[k]].h_res[slot[k]];
+    st[k + 1] = st[k] + n[k];
+    if (shard_res) shard_res[k] = rs[k];
+  }
+  combine_shards(st, rs.data(), nshards, out_offsets, res);
   return 0;
 }
 
@@ -980,6 +1224,20 @@ int vt_sharded_utf8_to_utf16(const uint8_t* in, uint64_t n, uint16_t* out, int n
 int vt_sharded_utf16_to_utf8(const uint16_t* in, uint64_t n, uint8_t* out, int ndev,
                              vt_result* res) {
   return sharded(in, n, out, ndev, 3, res, vt_split_point_utf16, vt_host_utf16_to_utf8);
+}
+
+int vt_sharded_device_utf8_to_utf16(int nshards, const int* dev, const uint8_t* const* d_in,
+                                    const uint64_t* n, uint16_t* const* d_out,
+                                    vt_result* shard_res, uint64_t* out_offsets, vt_result* res) {
+  return sharded_device(nshards, dev, d_in, n, d_out, shard_res, out_offsets, res,
+                        vt_utf8_to_utf16_async);
+}
+
+int vt_sharded_device_utf16_to_utf8(int nshards, const int* dev, const uint16_t* const* d_in,
+                                    const uint64_t* n, uint8_t* const* d_out,
+                                    vt_result* shard_res, uint64_t* out_offsets, vt_result* res) {
+  return sharded_device(nshards, dev, d_in, n, d_out, shard_res, out_offsets, res,
+                        vt_utf16_to_utf8_async);
 }
 
 int vt_gen_sizes(int cfg, uint64_t seed, uint64_t chunk0, uint64_t nchunks, uint64_t* d_sizes,
@@ -1021,7 +1279,9 @@ uint64_t vt_launch_count(void) { return g_launches.load(); }
 int vt_debug_probe(vt_stream stream, uint64_t* out5) {
   int dev;
   VT_TRY(current_device(dev));
-  Scratch* sc = scratch_for(dev, (cudaStream_t)stream);
+  std::shared_ptr<Scratch> hold;
+  VT_TRY(scratch_for(dev, (cudaStream_t)stream, hold));
+  Scratch* sc = hold.get();
   if (!sc->ctl) return VT_E_ARG;
   VT_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   VT_TRY(cudaMemcpy(out5, sc->ctl->pad, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost));

@@ -40,11 +40,15 @@ void force_emulated_backend(bool force) { g_force_emulated.store(force); }
 
 bool native_backend_available() { return vt_device_count() > 0; }
 
-TranscodeResult utf8_to_utf16(std::span<const uint8_t> input, uint16_t* out, bool /*validate*/,
+TranscodeResult utf8_to_utf16(std::span<const uint8_t> input, uint16_t* out, bool validate,
                               PathCounters* counters) {
   if (counters) counters->total_bytes += input.size();
   vt_result r;
-  check(vt_host_utf8_to_utf16(input.data(), input.size(), out, &r), "utf8_to_utf16");
+  // validate=false: the non-validating kernel (same result on valid input,
+  // unspecified output on invalid input, proj/src/utf8_to_utf16.cpp:230-239)
+  check(validate ? vt_host_utf8_to_utf16(input.data(), input.size(), out, &r)
+                 : vt_host_utf8_to_utf16_nonvalidating(input.data(), input.size(), out, &r),
+        "utf8_to_utf16");
   return to_result(r);
 }
 

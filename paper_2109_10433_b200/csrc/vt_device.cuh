@@ -428,6 +428,33 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
   return wbase + x - v;
 }
 
+// One-barrier form: after the barrier every warp scans the (<= 32) warp sums
+// itself with shuffles instead of warp 0 scanning them behind a second barrier.
+// The caller must not reuse warp_sums before another barrier.
+template <int THREADS, class Sync = SyncAll>
+__device__ __forceinline__ unsigned block_excl_scan1(unsigned v, unsigned* warp_sums,
+                                                     unsigned& total) {
+  constexpr int NW = THREADS / 32;
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  Sync::sync();
+  unsigned t = lane < NW ? warp_sums[lane] : 0u;
+#pragma unroll
+  for (int o = 1; o < NW; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+    if (lane >= (unsigned)o) t += y;
+  }
+  total = __shfl_sync(0xffffffffu, t, NW - 1);
+  const unsigned wbase = __shfl_sync(0xffffffffu, t, (wid + 31) & 31);
+  return (wid ? wbase : 0u) + x - v;
+}
+
 template <int THREADS, class Sync = SyncAll>
 __device__ __forceinline__ unsigned block_min(unsigned v, unsigned* scratch) {
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

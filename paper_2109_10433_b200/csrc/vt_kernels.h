@@ -50,6 +50,8 @@ constexpr int kModeValidate = 0, kModeTranscode = 1, kModeTranscodeBE = 2, kMode
 // length only: the validate kernel counting output elements (UTF-16 units of a
 // UTF-8 input, UTF-8 bytes of a UTF-16 input) instead of code points
 constexpr int kModeLength = 4;
+// UTF-8 -> UTF-16LE without validation (the reference's validate=false)
+constexpr int kModeTranscodeNV = 5;
 
 int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf8(bool transcode);
@@ -64,6 +66,11 @@ unsigned rows_utf16(unsigned long long head, unsigned long long n);
 // Batched validation of many short strings (one warp per string).
 int launch_validate_utf8_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
                                int64_t* first_err, cudaStream_t s);
+// Batched transcoding of many short strings (one thread per string, k_batch.cu)
+int launch_utf8_to_utf16_batch(const uint8_t* data, const uint64_t* offsets, uint64_t count,
+                               uint16_t* out, vt_result* res, int validate, cudaStream_t s);
+int launch_utf16_to_utf8_batch(const uint16_t* data, const uint64_t* offsets, uint64_t count,
+                               uint8_t* out, vt_result* res, cudaStream_t s);
 // skip value meaning "nothing of this chunk is scanned" (the stream failed)
 constexpr unsigned kSkipAll = 0xFFFFFFFFu;
 // Streaming UTF-8 validation (k_stream.cu): seam check before, carry/error

@@ -33,6 +33,17 @@ namespace vt {
 #define VT_GRAB_AT_U16 10  // cfg3 A/B (r1n): 8 1.100, 9 1.087, 10 1.077, 11 1.082, 12 1.081 ms
 #endif
 
+#ifndef VT_SCAN1
+#define VT_SCAN1 0  // one-barrier block scan (block_excl_scan1)
+#endif
+// VT_GRAB_EARLY: thread 0 takes the next tile before the copy-out of the
+// previous one and publishes it before the "buffer free" barrier, so the
+// loop-top barrier goes away (1: the look-back warp still gets the tile after
+// the decode; 2: right after that barrier)
+#ifndef VT_GRAB_EARLY
+#define VT_GRAB_EARLY 0
+#endif
+
 #ifndef VT_COMPUTE_THREADS
 #define VT_COMPUTE_THREADS 256
 #endif
@@ -220,7 +231,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       VT_PH(3);
     };
     while (true) {
-      ComputeSync::sync();
+      // (early grab: from the third tile on, the tile id was published before
+      // the previous tile's buffer-free barrier)
+      if (!VT_GRAB_EARLY || NS != 1 || j <= 1) ComputeSync::sync();
       VT_PH(0);
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase_sub[2], (unsigned long long)ph_t);
@@ -244,10 +257,21 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase_sub[3], (unsigned long long)ph_t);
 #endif
+      unsigned grabbed = 0;
+      const bool early = VT_GRAB_EARLY && NS == 1 && j > 0;
       if (NS == 1 && j > 0) {
+        if (early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
         copy_prev();
-        ComputeSync::sync();  // the buffer is free
+        if (early && threadIdx.x == 0) {
+          unsigned t = grabbed;
+          if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
+            t = a.ntiles;
+          sm.tile = t;
+          sm.lb_tile[(j + 1) & 3] = t;
+        }
+        ComputeSync::sync();  // the buffer is free (and the next tile id is out)
         VT_PH(4);
+        if (early && VT_GRAB_EARLY == 2) bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
       }
       // thread 0 takes the next tile from inside the decode (the codec says
       // where: Codec::emit calls `grab`); measured per codec, ms/GiB:
@@ -255,15 +279,16 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       //   1.270, before the decode: 1.261);
       //   UTF-8 -> UTF-16 at the end of the decode (after 12-15: +0.1-0.4 %,
       //   after 4 / 8: +0.9 %, before: +1.7 %)
-      unsigned grabbed = 0;
-      auto grab = [&]() { atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed); };
+      auto grab = [&]() {
+        if (!early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
+      };
 #ifndef VT_EXP_NOEMIT
       C::emit(a, tc, sm.out[j % NS], off, grab);
 #else
       grab();
 #endif
       VT_PH(5);
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && !early) {
         // (the error word was read at the top of the tile: one round trip
         // less on the path every warp waits for at the loop-top barrier)
         unsigned t = grabbed;
@@ -272,7 +297,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         sm.tile = t;
         sm.lb_tile[(j + 1) & 3] = t;
       }
-      bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
+      if (!(early && VT_GRAB_EARLY == 2)) bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
       VT_PH(6);
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase[7], 1ull);

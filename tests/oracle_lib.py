@@ -87,6 +87,36 @@ class Oracle:
         self._exh = L.fn("exhaustive_short_verdicts", C.c_uint64, _u8p)
         self._enc8 = L.fn("encode_utf8", C.c_uint32, C.c_uint32, _u8p)
         self._enc16 = L.fn("encode_utf16", C.c_uint32, C.c_uint32, _u16p)
+        self._b8 = L.fn("utf8_to_utf16_batch", None, _u8p, C.c_void_p, C.c_uint64, _u16p, C.c_void_p)
+        self._b16 = L.fn("utf16_to_utf8_batch", None, _u16p, C.c_void_p, C.c_uint64, _u8p, C.c_void_p)
+        self._fz = L.fn("fuzz_cases", C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, _u8p, C.c_void_p,
+                        C.c_uint64)
+
+    def fuzz_cases(self, seed: int, count: int, max_len: int):
+        """(data, offsets): `count` packed cases shaped like the reference's
+        run_fuzz (proj/src/harness.cpp:388-436)."""
+        cap = count * (max_len + 8) + 16
+        data = np.zeros(cap, dtype=np.uint8)
+        offs = np.zeros(count + 1, dtype=np.uint64)
+        tot = int(self._fz(seed, count, max_len, _p8(data), offs.ctypes.data, cap))
+        assert tot != 0xFFFFFFFFFFFFFFFF
+        return data[:tot].copy(), offs
+
+    def utf8_to_utf16_batch(self, data, offsets):
+        """Per-string scalar transcoding; outputs at the strings' offsets (units).
+        Returns (out, results[count, 3] as int64: consumed, written, error_at)."""
+        count = len(offsets) - 1
+        out = np.zeros(max(1, int(offsets[-1])) + 8, dtype=np.uint16)
+        res = np.zeros((count, 3), dtype=np.int64)
+        self._b8(_p8(data), offsets.ctypes.data, count, _p16(out), res.ctypes.data)
+        return out, res
+
+    def utf16_to_utf8_batch(self, units, offsets):
+        count = len(offsets) - 1
+        out = np.zeros(3 * max(1, int(offsets[-1])) + 16, dtype=np.uint8)
+        res = np.zeros((count, 3), dtype=np.int64)
+        self._b16(_p16(units), offsets.ctypes.data, count, _p8(out), res.ctypes.data)
+        return out, res
 
     def utf8_to_utf16(self, data, threads: int = 1):
         a = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data
