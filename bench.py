@@ -341,7 +341,7 @@ def round_trip_weak(vt, torch, dist, rank, world, steps, peak):
     equal = bool(r1.error_at is None and r2.error_at is None and r2.written == n
                  and torch.equal(d8[:n], d_in[:n]))
     ok = torch.tensor([1 if equal else 0], device="cuda")
-    gres, total_in = r2, n
+    gres, total_in = r1, n
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
