@@ -147,6 +147,8 @@ def lib():
         "vt_build_info": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("VT_LIB") and not hasattr(L, name):
+            continue  # an older experimental build (A/B tooling) may lack newer entry points
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args
@@ -181,8 +183,11 @@ def _ptr(a: np.ndarray) -> int:
 def utf8_to_utf16(data, validate: bool = True) -> tuple[np.ndarray, TranscodeResult]:
     """vtrans::utf8_to_utf16 vector overload (proj/include/vtrans/utf8_to_utf16.hpp:32-33).
 
-    ``validate`` is accepted for parity; the GPU always validates (allowed: the
-    reference leaves non-validating output on invalid input unspecified)."""
+    ``validate=False`` runs the non-validating kernel (the reference's
+    validate=false path: same result on valid input, unspecified output on
+    invalid input)."""
+    if not validate:
+        return utf8_to_utf16_nonvalidating(data)
     a = _bytes_view(data)
     out = np.empty(len(a) + 8, dtype=np.uint16)
     r = _CRes()

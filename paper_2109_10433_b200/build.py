@@ -45,9 +45,21 @@ def _deps() -> list[str]:
     return files
 
 
+STAMP = os.path.join(LIBDIR, "build_flags.txt")
+
+
+def _flags() -> str:
+    """The flags that change the build (an experimental VT_NVCC_EXTRA build
+    must never pass for the product library)."""
+    return " ".join([*ARCH, os.environ.get("VT_NVCC_EXTRA", "")]).strip()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
+    with open(STAMP) as f:
+        if f.read() != _flags():
+            return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(f) <= t for f in _deps())
 
@@ -91,6 +103,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(" ".join(link) + "\n" + p.stdout + p.stderr)
         raise RuntimeError("link of libvtrans_gpu.so failed")
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flags())
     if verbose:
         print("\n".join(logs))
     return LIB

@@ -170,13 +170,36 @@ __device__ __noinline__ unsigned generic_units(const Words16& W, unsigned lo, un
       }
       unsigned len;
       const uint32_t p = encode_unit(u, pv, len);
-      if (dst)
+      if (dst) {
+        VT_CHECK_STS(smem_addr(dst + q), len);
         for (unsigned b = 0; b < len; b++) dst[q + b] = (uint8_t)(p >> (8 * b));
+      }
       q += len;
     }
     pw = cw;
   }
   return q;
+}
+
+// UTF-8 bytes (or code points) of units [lo, lim) of a thread's window, for a
+// range of whole valid characters (bytes per unit as in classify16: 1 +
+// [>= 0x80] + [>= 0x800] - [surrogate]; code points: units minus low
+// surrogates).  SWAR with a lane-range mask per word, for the error path.
+__device__ __noinline__ unsigned swar_count16(const Words16 W, unsigned lo, unsigned lim, bool bytes) {
+  unsigned cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K16_WPT; k++) {
+    const uint32_t x = W.w[k + 1];
+    const unsigned i = 2 * k;
+    const uint32_t m = (i >= lo && i < lim ? 0x00008000u : 0u) | (i + 1 >= lo && i + 1 < lim ? 0x80000000u : 0u);
+    const uint32_t x15 = x & 0x7FFF7FFFu;
+    const uint32_t sr = sur16(x);
+    if (bytes)
+      cnt += __popc(m) + __popc(ge80_16(x, x15) & m) + __popc(ge800_16(x, x15) & m) - __popc(sr & m);
+    else
+      cnt += __popc(m) - __popc(sr & (x << 5) & m);
+  }
+  return cnt;
 }
 
 struct TileCount16 {
@@ -300,12 +323,10 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
     if (threadIdx.x == 0) {
       const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
       atomicMin(&a.ctl->err, pos);
+      VT_TR_MIN(1);
     }
   }
-  {
-    const Words16 tmp = tc.W;
-    tc.cnt = generic_units(tmp, tc.lo, tc.lim, kTranscode, nullptr);
-  }
+  tc.cnt = swar_count16(tc.W, tc.lo, tc.lim, kTranscode);
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
@@ -325,6 +346,30 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
 //    next unit's bytes go and are overwritten by them (same thread, program
 //    order).  Only the thread's last word may not spill (the bytes after it
 //    belong to the next thread): it takes the predicated form.
+// The 2nd / 3rd byte stores of the overlapping form are predicated on the
+// unit needing them (non-ASCII / 3-byte): fewer shared-memory wavefronts for
+// one LOP3 per store (the kernel is bound by the ALU pipe and the shared-memory
+// data pipe together: ALU 79 %, L1/shared 77 %).  r2h A/B, cfg3: 1.095 ->
+// 1.080 ms (both), 1.081 (3rd byte only).
+#ifndef VT_U16_PRED_S
+#define VT_U16_PRED_S 1
+#endif
+#ifndef VT_U16_PRED_T
+#define VT_U16_PRED_T 1
+#endif
+// Byte store at a when `plane` has bit MASK set (the test goes straight into
+// the predicate, one LOP3).
+template <uint32_t MASK>
+__device__ __forceinline__ void sts8_if(uint32_t a, uint32_t v, uint32_t plane) {
+  VT_CHECK_STS(a, 1);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d;\n\t"
+      "lop3.or.b32 d|p, %1, 0, %2, 0xA0, 0;\n\t"  // a & c
+      "@p st.shared.u8 [%0], %3;\n\t}"
+      :
+      : "r"(a), "r"(plane), "n"(MASK), "r"(v));
+}
+
 template <bool kOverlap>
 __device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t& q, uint32_t K80,
                                                uint32_t KE0, uint32_t K58) {
@@ -363,11 +408,27 @@ __device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t
   const uint32_t T = lop3<0xEA>(x, 0x003F003Fu, K80);
   const uint32_t S = lop3<0xEA>(lop3<0xCA>(m3, x6, lop3<0xCA>(mh, w >> 2, x)), 0x003F003Fu, K80);
   if (kOverlap) {
+#if VT_U16_PRED_S
+    sts8_if<0x00008000u>(q + 1, S, g80);
+#else
     sts8(q + 1, S);
+#endif
+#if VT_U16_PRED_T
+    sts8_if<0x00008000u>(q + 2, T, is3);
+#else
     sts8(q + 2, T);
+#endif
     sts8(q1, F1);
+#if VT_U16_PRED_S
+    sts8_if<0x80000000u>(q1 + 1, S >> 16, g80);
+#else
     sts8(q1 + 1, S >> 16);
+#endif
+#if VT_U16_PRED_T
+    sts8_if<0x80000000u>(q1 + 2, T >> 16, is3);
+#else
     sts8(q1 + 2, T >> 16);
+#endif
   } else {
     const uint32_t n0 = n & 0xFFFFu, n1 = n >> 16;
     if (n0 >= 2) sts8(q + 1, S);
@@ -447,14 +508,16 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
   const unsigned long long nrows = (unsigned long long)(end + K16_ROW - 1) / K16_ROW;
   const Src16 src{a.base, a.head, a.n, kBE};
   unsigned long long total = 0;
-  unsigned it = 0;
-  for (unsigned long long row = gw; row < nrows; row += nwarps, it++) {
+  unsigned wtot = 0;  // this warp's running total (rows so far)
+  if (threadIdx.x == 0) VT_TR_MIN(8);
+  // Stop behind a known error (warp-uniform).  The error word is loaded at the
+  // top of every row and tested at the top of the next one, so the check adds
+  // no latency and a warp runs at most one row past a found error.
+  unsigned long long e_prev = kNoError;
+  for (unsigned long long row = gw; row < nrows; row += nwarps) {
     const long long r0 = (long long)row * K16_ROW;
-    if ((it & 3) == 0) {  // stop behind a known error (warp-uniform decision)
-      unsigned long long e = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
-      e = __shfl_sync(0xffffffffu, e, 0);
-      if (e != kNoError && (long long)e + head < r0) break;
-    }
+    if (e_prev != kNoError && (long long)e_prev + head < r0) break;
+    const unsigned long long e_next = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
     const long long v0 = r0 + (long long)K16_UPT * lane;
     const bool interior = r0 - 2 >= head && r0 + K16_ROW + 2 <= end;
     Words16 W;
@@ -478,13 +541,19 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
       const Words16 tmp = W;
       const unsigned er = first_error16(tmp, lo, hi);
-      if (er != kNone16) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
-      cnt = generic_units(tmp, lo, hi, kUnits, nullptr);
+      if (er != kNone16) {
+        atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
+        VT_TR_MIN(1);
+      }
+      cnt = swar_count16(W, lo, er != kNone16 ? er : hi, kUnits);
     }
     total += cnt;
     const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) row_counts[row] = rc;
+    wtot += rc;
+    if (lane == 0) row_counts[row] = wtot;
+    e_prev = __shfl_sync(0xffffffffu, e_next, 0);
   }
+  if (lane == 0) VT_TR_MAX(9);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
   if (lane == 0) warp_tot[wib] = total;
@@ -498,14 +567,13 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
   }
   __syncthreads();
   if (!last) return;
+  if (threadIdx.x == 0) VT_TR_MAX(10);
   __threadfence();
   const unsigned long long e = load_relaxed(&a.ctl->err);
   unsigned long long written = load_relaxed(&a.ctl->count);
   if (e != kNoError) {
     const unsigned long long erow = (e + a.head) / K16_ROW;
-    unsigned long long t = 0;
-    for (unsigned long long r = threadIdx.x; r < erow; r += blockDim.x)
-      t += ((volatile unsigned*)row_counts)[r];
+    unsigned long long t = prefix_rows(row_counts, erow, nwarps);
     if (wib == 0) {
       const long long v0 = (long long)erow * K16_ROW + (long long)K16_UPT * lane;
       const long long stop = (long long)e + head;
@@ -513,7 +581,7 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
       const unsigned lim = (unsigned)max((long long)lo, min((long long)K16_UPT, stop - v0));
       Words16 tmp;
       load_edge16<kBE>(src, v0, tmp.w);
-      t += generic_units(tmp, lo, lim, kUnits, nullptr);
+      t += swar_count16(tmp, lo, lim, kUnits);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -533,6 +601,7 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
     a.ctl->err = kNoError;
     __threadfence();
     a.ctl->done = 0;
+    VT_TR_MAX(11);
   }
 }
 
@@ -590,6 +659,16 @@ int occupancy_utf16(bool transcode) {
   }
   return n;
 }
+
+#ifdef VT_TRACE
+int read_trace16(unsigned long long* out16) {
+  int rc = (int)cudaMemcpyFromSymbol(out16, g_trace, sizeof(g_trace));
+  unsigned long long init[16];
+  for (int i = 0; i < 16; i++) init[i] = (i == 0 || i == 1 || i == 8) ? ~0ull : 0ull;
+  if (!rc) rc = (int)cudaMemcpyToSymbol(g_trace, init, sizeof(init));
+  return rc;
+}
+#endif
 
 #ifdef VT_PHASES
 int read_phases16(unsigned long long* out8) {

@@ -100,9 +100,24 @@ __device__ __forceinline__ unsigned b12(uint32_t pw, uint32_t cw, uint32_t nw, i
 // error), out of line, on a copy of the caller's window (so the hot path keeps
 // its words in registers); one loop step per word with the words before and
 // after in registers.
+//
+// The scan starts 3 bytes before the first lane where the lead/continuation
+// planes disagree or a special lead fails its range check (first_violation):
+// no rule-A error lies further back -- an orphan continuation is itself such a
+// lane, a lead that fails to decode either fails its range check at its own
+// lane or leaves one of its next 3 lanes short of a continuation (the argument
+// in classify) -- so the per-byte loop runs over a few bytes instead of 64
+// (the loop is serial: ~40 dependent steps per byte on one thread, which the
+// whole tile waits for).
+__device__ __forceinline__ unsigned long long need_plane(uint32_t l2, uint32_t l3, uint32_t l4);
+__device__ __noinline__ unsigned first_violation(const Words& W);
+
 __device__ __noinline__ unsigned first_error_w(const Words& W, unsigned lo, unsigned hi) {
-  uint32_t pw = W.w[0], cw = W.w[1];
-  for (int k = 0; k < K8_WPT; k++) {
+  const unsigned v = first_violation(W);
+  if (v != kNone && v >= 3 && v - 3 > lo) lo = v - 3;
+  const int k0 = (int)(lo >> 2);
+  uint32_t pw = W.w[k0], cw = W.w[k0 + 1];
+  for (int k = k0; k < K8_WPT; k++) {
     const uint32_t nw = W.w[k + 2];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -264,6 +279,41 @@ __device__ __forceinline__ ClassOut classify_nv(const Words& W) {
   return o;
 }
 
+// First lane (0..63 own bytes, 64..66 the next word's) where the summed
+// requirement plane and the continuation plane differ, or a special lead's
+// range check fails (the planes of classify / specials_check); kNone if none.
+__device__ __noinline__ unsigned first_violation(const Words& W) {
+  uint32_t carry;
+  {
+    const uint32_t x = W.w[0], x2 = x << 1;
+    const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
+    carry = (uint32_t)(need_plane(l2, l3, l4) >> 32);
+  }
+  for (int k = 1; k <= K8_WPT + 1; k++) {
+    const uint32_t x = W.w[k], x2 = x << 1;
+    const uint32_t c = x & ~x2 & H;
+    const uint32_t l2 = x & x2 & H, l3 = l2 & (x << 2), l4 = l3 & (x << 3);
+    const unsigned long long t = need_plane(l2, l3, l4);
+    const uint32_t need = (uint32_t)t + carry;
+    carry = (uint32_t)(t >> 32);
+    uint32_t bad = (need ^ c) & H;
+    if (k <= K8_WPT) {
+      const uint32_t x7 = x & 0x7F7F7F7Fu;
+      const uint32_t ge_c2 = x7 + 0x3E3E3E3Eu, ge_e1 = x7 + 0x1F1F1F1Fu;
+      const uint32_t ge_ed = x7 + 0x13131313u, ge_ee = x7 + 0x12121212u;
+      const uint32_t ge_f1 = x7 + 0x0F0F0F0Fu, ge_f4 = x7 + 0x0C0C0C0Cu, ge_f5 = x7 + 0x0B0B0B0Bu;
+      const uint32_t n1 = prmt(x, W.w[k + 1], 0x4321);
+      const uint32_t b5 = n1 << 2, b45 = (n1 | (n1 << 1)) << 2;
+      bad |= ((l2 & ~ge_c2) | (l3 & ~ge_e1 & ~b5) | (l3 & ge_ed & ~ge_ee & b5) | (l4 & ~ge_f1 & ~b45) |
+              (l4 & ge_f4 & ~ge_f5 & b45) | (l4 & ge_f5)) & H;
+    } else {
+      bad &= 0x00808080u;  // only the next word's lanes 0..2 can concern our bytes
+    }
+    if (bad) return 4u * (k - 1) + ((unsigned)__ffs(bad) - 1u) / 8u;
+  }
+  return kNone;
+}
+
 // ---- generic path (ends of the input, tiles with an error): rare, per byte --
 // Counts (units or characters) of the characters starting at positions
 // [lo, lim) of the thread's bytes; with `dst`, also writes their units.
@@ -293,12 +343,16 @@ __device__ __noinline__ unsigned generic_chars(const Words& W, unsigned lo, unsi
       if (!units) {
         q++;
       } else if (cp < 0x10000u) {
-        if (dst) dst[q] = be ? bswap16(cp) : (uint16_t)cp;
+        if (dst) {
+          VT_CHECK_STS(smem_addr(dst + q), 2);
+          dst[q] = be ? bswap16(cp) : (uint16_t)cp;
+        }
         q++;
       } else {
         const unsigned s = cp - 0x10000u;
         if (dst) {
           const unsigned h = 0xD800u + (s >> 10), l = 0xDC00u + (s & 0x3FFu);
+          VT_CHECK_STS(smem_addr(dst + q), 4);
           dst[q] = be ? bswap16(h) : (uint16_t)h;
           dst[q + 1] = be ? bswap16(l) : (uint16_t)l;
         }
@@ -311,9 +365,29 @@ __device__ __noinline__ unsigned generic_chars(const Words& W, unsigned lo, unsi
   return q;
 }
 
+// Characters (or UTF-16 units) starting at positions [lo, lim) of a thread's
+// window, for a range of whole valid characters (the valid prefix of a tile
+// with an error, an end tile): non-continuation bytes in range, plus one per
+// 4-byte lead for units.  SWAR with a lane-range mask per word; it replaced
+// the per-byte generic_chars count on the error path (the tile waits for it).
+__device__ __noinline__ unsigned swar_count(const Words W, unsigned lo, unsigned lim, bool units) {
+  unsigned cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K8_WPT; k++) {
+    const uint32_t x = W.w[k + 1], x2 = x << 1;
+    const int s0 = min(max((int)lo - 4 * k, 0), 4), e0 = min(max((int)lim - 4 * k, 0), 4);
+    const uint32_t hi_m = e0 >= 4 ? 0xFFFFFFFFu : (1u << (8 * e0)) - 1u;
+    const uint32_t m = e0 <= s0 ? 0u : hi_m & ~((1u << (8 * s0)) - 1u);
+    cnt += __popc(~(x & ~x2) & H & m);
+    if (units) cnt += __popc(x & x2 & (x << 2) & (x << 3) & H & m);
+  }
+  return cnt;
+}
+
 // Predicated 16-bit store at q, q += 2, when (~c | c2) has bit MASK set.
 template <uint32_t MASK>
 __device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t c2, uint32_t v) {
+  if (VT_CHECKS && ((~c | c2) & MASK)) VT_CHECK_STS(q, 2);
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 d;\n\t"
       "lop3.or.b32 d|p, %1, %2, %3, 0x8A, 0;\n\t"  // (~a | b) & c
@@ -335,6 +409,7 @@ __device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t 
 #endif
 __device__ __forceinline__ void sts16x4_if_lead(uint32_t& q, uint32_t c, uint32_t c2, uint32_t u01,
                                                 uint32_t u23) {
+  if (VT_CHECKS) VT_CHECK_STS(q, 2 * __popc((~c | c2) & 0x80808080u));
   asm volatile(
       "{\n\t.reg .pred p0, p1, p2, p3;\n\t.reg .b32 d0, d1, d2, d3, h1, h3;\n\t"
       "lop3.or.b32 d0|p0, %1, %2, 0x00000080, 0x8A, 0;\n\t"
@@ -397,9 +472,9 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
 // stores per word, not 8).  `carry4` (bit 7) says the previous word's lane 3
 // was a 4-byte lead of this thread; a lead in the thread's last byte has its
 // ls lane in the next thread and is finished by emit_tail_ls.
-template <bool kBE, bool kNV = false>
+template <bool kBE, bool kNV = false, bool kMasked = false>
 __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t& q,
-                                               uint32_t& carry4, uint32_t KDC) {
+                                               uint32_t& carry4, uint32_t KDC, uint32_t range = ~0u) {
   const uint32_t n1 = prmt(c, n, 0x4321);  // byte i = b[i+1]
   const uint32_t n2 = prmt(c, n, 0x5432);  // byte i = b[i+2]
   const uint32_t c2 = c << 1;
@@ -433,7 +508,9 @@ __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t&
   u23 = lop3<0xCA>(prmt(m4, 0, 0x3322), hs23, u23);
   // (non-validating: an ls lane stores only if it is a continuation, so the
   // stores match classify_nv's count on any input)
-  const uint32_t st7 = kNV ? lead7 | (ls7 & c & ~c2) : lead7 | ls7;
+  // (kMasked: only characters starting in the lanes `range` selects -- the
+  // valid prefix of a tile with an error, the input part of an end tile)
+  const uint32_t st7 = (kNV ? lead7 | (ls7 & c & ~c2) : lead7 | ls7) & (kMasked ? range : ~0u);
   if (st7 & 0x00000080u) { sts16(q, u01); q += 2; }
   if (st7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
   if (st7 & 0x00800000u) { sts16(q, u23); q += 2; }
@@ -531,12 +608,10 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     if (threadIdx.x == 0) {
       const unsigned long long pos = (unsigned long long)(vt0 + tile_err) - a.head;
       atomicMin(&a.ctl->err, pos);
+      VT_TR_MIN(1);
     }
   }
-  {
-    const Words tmp = tc.W;
-    tc.cnt = generic_chars(tmp, tc.lo, tc.lim, kTranscode, nullptr);
-  }
+  tc.cnt = swar_count(tc.W, tc.lo, tc.lim, kTranscode);
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
@@ -572,9 +647,23 @@ __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, 
         emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
     }
   } else {
+    // a tile with an error: the same SWAR decode (4-byte-capable form), its
+    // stores limited to the characters starting in [lo, lim) -- whole valid
+    // characters, the count swar_count gave (the per-byte generic path this
+    // replaced kept the whole tile waiting ~20 us)
     mid();
-    const Words tmp = tc.W;
-    generic_chars(tmp, tc.lo, tc.lim, true, stage + off, kBE);
+    uint32_t q = smem_addr(stage) + 2u * off;
+    uint32_t carry4 = 0, KDC = 0xDCDCDCDCu;
+    asm volatile("" : "+r"(KDC));
+#pragma unroll
+    for (int k = 1; k <= K8_WPT; k++) {
+      const int s0 = min(max((int)tc.lo - 4 * (k - 1), 0), 4), e0 = min(max((int)tc.lim - 4 * (k - 1), 0), 4);
+      const uint32_t hi_m = e0 >= 4 ? 0xFFFFFFFFu : (1u << (8 * e0)) - 1u;
+      const uint32_t m = e0 <= s0 ? 0u : hi_m & ~((1u << (8 * s0)) - 1u);
+      emit_word_four<kBE, kNV, true>(tc.W.w[k], tc.W.w[k + 1], q, carry4, KDC, m);
+    }
+    // (a 4-byte lead in the last byte finishes its pair only if it is in range)
+    if (carry4 && tc.lim >= (unsigned)K8_BPT) emit_tail_ls<kBE>(tc.W.w[K8_WPT + 1], q);
   }
 }
 
@@ -638,14 +727,16 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
   const unsigned long long nrows = (unsigned long long)(end + K8_ROW - 1) / K8_ROW;
   const Src src{a.base, a.head, a.n};
   unsigned long long total = 0;
-  unsigned it = 0;
-  for (unsigned long long row = gw; row < nrows; row += nwarps, it++) {
+  unsigned wtot = 0;  // this warp's running total (rows so far)
+  if (threadIdx.x == 0) VT_TR_MIN(8);
+  // Stop behind a known error (warp-uniform).  The error word is loaded at the
+  // top of every row and tested at the top of the next one, so the check adds
+  // no latency and a warp runs at most one row past a found error.
+  unsigned long long e_prev = kNoError;
+  for (unsigned long long row = gw; row < nrows; row += nwarps) {
     const long long r0 = (long long)row * K8_ROW;
-    if ((it & 3) == 0) {  // stop behind a known error (warp-uniform decision)
-      unsigned long long e = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
-      e = __shfl_sync(0xffffffffu, e, 0);
-      if (e != kNoError && (long long)e + head < r0) break;
-    }
+    if (e_prev != kNoError && (long long)e_prev + head < r0) break;
+    const unsigned long long e_next = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
     const long long v0 = r0 + (long long)K8_BPT * lane;
     const bool interior = r0 - 4 >= head && r0 + K8_ROW + 4 <= end;
     Words W;
@@ -665,14 +756,22 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
       const Words tmp = W;
       const unsigned er = first_error_w(tmp, lo, hi);
-      if (er != kNone) atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
-      cnt = generic_chars(tmp, lo, hi, kUnits, nullptr);
+      if (er != kNone) {
+        atomicMin(&a.ctl->err, (unsigned long long)(v0 + er - head));
+        VT_TR_MIN(1);
+      }
+      // (exact only up to the error, which is all the finalize uses of a row
+      // that holds one)
+      cnt = swar_count(W, lo, er != kNone ? er : hi, kUnits);
     }
     total += cnt;
     const unsigned rc = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) row_counts[row] = rc;
+    wtot += rc;
+    if (lane == 0) row_counts[row] = wtot;
+    e_prev = __shfl_sync(0xffffffffu, e_next, 0);
   }
   // per-CTA total, one atomic
+  if (lane == 0) VT_TR_MAX(9);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
   if (lane == 0) warp_tot[wib] = total;
@@ -686,15 +785,14 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
   }
   __syncthreads();
   if (!last) return;
+  if (threadIdx.x == 0) VT_TR_MAX(10);
   __threadfence();
   const unsigned long long e = load_relaxed(&a.ctl->err);
   unsigned long long written = load_relaxed(&a.ctl->count);
   if (e != kNoError) {
     // valid prefix: rows before the error row, then the error row up to e
     const unsigned long long erow = (e + a.head) / K8_ROW;
-    unsigned long long t = 0;
-    for (unsigned long long r = threadIdx.x; r < erow; r += blockDim.x)
-      t += ((volatile unsigned*)row_counts)[r];
+    unsigned long long t = prefix_rows(row_counts, erow, nwarps);
     if (wib == 0) {
       const long long v0 = (long long)erow * K8_ROW + (long long)K8_BPT * lane;
       const long long stop = (long long)e + head;
@@ -702,7 +800,7 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
       const unsigned lim = (unsigned)max((long long)lo, min((long long)K8_BPT, stop - v0));
       Words tmp;
       load_edge(src, v0, tmp.w);
-      t += generic_chars(tmp, lo, lim, kUnits, nullptr);
+      t += swar_count(tmp, lo, lim, kUnits);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -722,6 +820,7 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
     a.ctl->err = kNoError;
     __threadfence();
     a.ctl->done = 0;
+    VT_TR_MAX(11);
   }
 }
 
@@ -782,6 +881,17 @@ int occupancy_utf8(bool transcode) {
   }
   return n;
 }
+
+#ifdef VT_TRACE
+// reads and re-arms this translation unit's trace stamps (mins start at ~0)
+int read_trace8(unsigned long long* out16) {
+  int rc = (int)cudaMemcpyFromSymbol(out16, g_trace, sizeof(g_trace));
+  unsigned long long init[16];
+  for (int i = 0; i < 16; i++) init[i] = (i == 0 || i == 1 || i == 8) ? ~0ull : 0ull;
+  if (!rc) rc = (int)cudaMemcpyToSymbol(g_trace, init, sizeof(init));
+  return rc;
+}
+#endif
 
 #ifdef VT_PHASES
 int read_phases(unsigned long long* out8) {

@@ -25,6 +25,16 @@
 #include "vt_device.cuh"
 #include "vt_kernels.h"
 
+#ifdef VT_TRACE
+namespace vt {
+int read_trace8(unsigned long long* out16);
+int read_trace16(unsigned long long* out16);
+}  // namespace vt
+extern "C" int vt_debug_trace(int utf16, uint64_t* out16) {
+  return utf16 ? vt::read_trace16(reinterpret_cast<unsigned long long*>(out16))
+               : vt::read_trace8(reinterpret_cast<unsigned long long*>(out16));
+}
+#endif
 #ifdef VT_PHASES
 namespace vt {
 int read_phases(unsigned long long* out8);
@@ -115,6 +125,7 @@ struct Scratch {
   size_t rows_cap = 0;
 };
 
+// Per-row running totals of the validate kernels (prefix_rows).
 int ensure_rows(Scratch& sc, cudaStream_t s, size_t rows) {
   if (rows <= sc.rows_cap) return 0;
   VT_TRY(cudaStreamSynchronize(s));  // the old array may still be in use
@@ -245,6 +256,7 @@ int run_utf8_locked(Scratch* sc, const DeviceInfo& di, const uint8_t* d_in, uint
   a.dbg = dbg;
   a.skip = d_skip;
   a.rows = nullptr;
+  a.out_cap = 2 * n;  // the contract: n units
   if (!transcode) {
     const unsigned rows = vt::rows_utf8(a.head, n);
     VT_TRY(ensure_rows(*sc, s, rows));
@@ -272,6 +284,7 @@ int run_utf16_locked(Scratch* sc, const DeviceInfo& di, const uint16_t* d_in, ui
   a.n = n;
   a.ntiles = vt::tiles_utf16(a.head, n);
   a.rows = nullptr;
+  a.out_cap = 3 * n + 16;  // the contract: 3n + 16 bytes
   if (!transcode) {
     const unsigned rows = vt::rows_utf16(a.head, n);
     VT_TRY(ensure_rows(*sc, s, rows));
@@ -428,6 +441,84 @@ int ensure_pinned(uint8_t*& p, size_t& cap, size_t need) {
   return 0;
 }
 
+// Host copies between a caller's pageable buffer and the pinned staging of the
+// pipelined path, split over a small pool of persistent threads (one thread
+// moves ~5-10 GB/s; the pageable drop-in case -- a reference caller passing a
+// std::vector -- is bound by these copies, not by PCIe).  The calling thread
+// takes part; the pool is never destroyed (its workers idle at exit).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();
+    return *p;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < 2 * kPiece || nthreads_ == 0) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    auto job = std::make_shared<Job>();
+    job->dst = static_cast<uint8_t*>(dst);
+    job->src = static_cast<const uint8_t*>(src);
+    job->bytes = bytes;
+    job->pieces = (bytes + kPiece - 1) / kPiece;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = job;
+      gen_++;
+    }
+    cv_.notify_all();
+    job->work();
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [&] { return job->done.load() == job->pieces; });
+  }
+
+ private:
+  static constexpr size_t kPiece = 1u << 20;
+  struct Job {
+    uint8_t* dst = nullptr;
+    const uint8_t* src = nullptr;
+    size_t bytes = 0, pieces = 0;
+    std::atomic<size_t> next{0}, done{0};
+    std::mutex mu;
+    std::condition_variable cv;
+    void work() {
+      size_t k;
+      while ((k = next.fetch_add(1)) < pieces) {
+        const size_t off = k * kPiece, len = std::min(kPiece, bytes - off);
+        std::memcpy(dst + off, src + off, len);
+        if (done.fetch_add(1) + 1 == pieces) {
+          std::lock_guard<std::mutex> lk(mu);
+          cv.notify_all();
+        }
+      }
+    }
+  };
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    nthreads_ = hw >= 4 ? std::min(7u, hw / 2) : 0u;
+    for (unsigned i = 0; i < nthreads_; i++)
+      std::thread([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::shared_ptr<Job> job;
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            job = job_;
+          }
+          job->work();
+        }
+      }).detach();
+  }
+  unsigned nthreads_ = 0;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  uint64_t gen_ = 0;
+  std::shared_ptr<Job> job_;
+};
+
 // Input elements per pipeline chunk (VT_PIPE_CHUNK_MB MiB of input).
 template <class In>
 constexpr uint64_t pipe_chunk() { return ((uint64_t)VT_PIPE_CHUNK_MB << 20) / sizeof(In); }
@@ -494,7 +585,7 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
     if (!pin_in) {
       // the staging buffer was last read by chunk k-3's copy, which finished
       // before its result was read
-      std::memcpy(c->ph_in[b], src, len * sizeof(In));
+      CopyPool::get().copy(c->ph_in[b], src, len * sizeof(In));
       src = reinterpret_cast<const In*>(c->ph_in[b]);
     }
     VT_TRY(cudaMemcpyAsync(c->pd_in[b], src, len * sizeof(In), cudaMemcpyHostToDevice, s));
@@ -532,7 +623,7 @@ int host_transcode_pipelined(HostCtx* c, const In* in, uint64_t n, Out* out,
         rc = (int)cudaMemcpyAsync(c->ph_out[b], c->pd_out[b], r.written * sizeof(Out),
                                   cudaMemcpyDeviceToHost, c->ps[b]);
         if (!rc) rc = (int)cudaStreamSynchronize(c->ps[b]);
-        if (!rc) std::memcpy(out + written, c->ph_out[b], r.written * sizeof(Out));
+        if (!rc) CopyPool::get().copy(out + written, c->ph_out[b], r.written * sizeof(Out));
       }
       if (rc) break;
     }

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda/atomic>
 
 #include "../../include/vtrans_gpu.h"
@@ -43,6 +44,59 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+// VT_TRACE builds (tools/cfg4_trace.py): global-timer stamps of the phases of
+// an early-error call, per translation unit (read with vt_debug_trace).
+#ifdef VT_TRACE
+static __device__ unsigned long long g_trace[16];
+__device__ __forceinline__ unsigned long long vt_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define VT_TR_MIN(i) atomicMin(&g_trace[i], vt_gtimer())
+#define VT_TR_MAX(i) atomicMax(&g_trace[i], vt_gtimer())
+#else
+#define VT_TR_MIN(i) \
+  do {               \
+  } while (0)
+#define VT_TR_MAX(i) \
+  do {               \
+  } while (0)
+#endif
+
+// VT_CHECKS builds (tools/gpu_checked.sh): every staging store and every
+// copy-out range is bounds-checked and traps with a message when out of range
+// (the pool has compute-sanitizer closed; this is the substitute).
+#ifndef VT_CHECKS
+#define VT_CHECKS 0
+#endif
+extern __shared__ __align__(16) uint8_t vt_dyn_smem[];
+// bytes of PipeSmem after its staging region (scan .. excl, vt_pipeline.cuh
+// static_asserts it): a staging store must land before them
+constexpr unsigned kPipeTail = 120;
+
+static __device__ __noinline__ void vt_check_fail(const char* what, unsigned long long a,
+                                                  unsigned long long b, unsigned long long lo,
+                                                  unsigned long long hi) {
+  printf("VT_CHECKS: %s [%llu, +%llu) outside [%llu, %llu) block %d thread %d\n", what, a, b, lo, hi,
+         blockIdx.x, threadIdx.x);
+  __trap();
+}
+
+static __device__ __forceinline__ void vt_check_sts(uint32_t a, unsigned bytes) {
+  uint32_t dsz;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+  const uint32_t lo = (uint32_t)__cvta_generic_to_shared(vt_dyn_smem), hi = lo + dsz - kPipeTail;
+  if (a < lo || a + bytes > hi) vt_check_fail("staging store", a, bytes, lo, hi);
+}
+#if VT_CHECKS
+#define VT_CHECK_STS(a, b) vt_check_sts((a), (b))
+#else
+#define VT_CHECK_STS(a, b) \
+  do {                     \
+  } while (0)
+#endif
+
 // A/B probes of the staging-store cost (timing only, output is garbage):
 // VT_EXP_LANESTS keeps every store but sends lane i to bank i (no conflicts).
 #ifdef VT_EXP_LANESTS
@@ -55,6 +109,7 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 #define VT_LANE_ADDR(a) (a)
 #endif
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  VT_CHECK_STS(a, 2);
   a = VT_LANE_ADDR(a);
 #ifdef VT_EXP_NOSTS
   asm volatile("" ::"r"(a), "r"(v));
@@ -66,6 +121,7 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 }
 __device__ __forceinline__ void sts8(uint32_t a, uint32_t v) {
   // stores the low byte of v (no masking instruction needed)
+  VT_CHECK_STS(a, 1);
   a = VT_LANE_ADDR(a);
 #ifdef VT_EXP_NOSTS
   asm volatile("" ::"r"(a), "r"(v));
@@ -180,7 +236,14 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
   // (not in the first two waves of tiles: small inputs are latency-bound)
   if (tile >= 2 * gridDim.x) __nanosleep(VT_LB_DELAY);
 #endif
-  while (true) {
+  for (bool first = true;; first = false) {
+    // a tile behind a known error is dead: give up (its output is never read;
+    // the tail of an early-error call waits on these look-backs).  Checked at
+    // the start, beside the first status loads (same round trip), and
+    // whenever a poll makes no progress (below); checking on every poll costs
+    // the hot path ~0.7 % (everyone hits the error word's line).
+    const unsigned long long err =
+        first && lane == 0 ? load_relaxed(const_cast<unsigned long long*>(&ctl->err)) : kNoError;
     unsigned long long v[K];
     bool rdy[K], pre[K];
 #pragma unroll
@@ -190,6 +253,10 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
       rdy[k] = idx < 0 || (((st >> 62) != 0) && (((st >> 48) & 0x3FFF) == ep));
       pre[k] = idx < 0 || (rdy[k] && (st >> 62) == 2);  // before tile 0: prefix 0
       v[k] = idx < 0 ? 0ull : (st & kValMask);
+    }
+    {
+      const unsigned long long e = __shfl_sync(0xffffffffu, err, 0);
+      if (e != kNoError && (e + head) / tile_bytes < tile) return ~0ull;
     }
     uint32_t wsum[K];  // window sums of the fully-ready windows passed so far
     int k = 0;
@@ -395,6 +462,28 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// ---- row bookkeeping of the barrier-free validate kernels --------------------
+// Warp gw takes rows gw, gw + nwarps, ... and stores, per row, its running
+// total (inclusive) of the counts of its own rows.  The last CTA of a call with
+// an error needs the count of the valid prefix: the rows before the error row
+// are, for every warp w, exactly its rows up to its last one before the error
+// row, so the sum is one stored running total per warp -- min(erow, nwarps)
+// independent loads spread over the CTA (reading every row count, one
+// dependent L2 round trip per 256 rows, made a late error cost tens of us).
+__device__ __forceinline__ unsigned long long prefix_rows(const unsigned* cum, unsigned long long erow,
+                                                          unsigned long long nwarps) {
+  if (erow == 0) return 0;
+  // warp w's last row before erow: w + nwarps * q0 if w <= (erow - 1) % nwarps,
+  // else one round earlier (rows of warps w >= erow do not exist)
+  const unsigned long long q0 = (erow - 1) / nwarps, r0 = (erow - 1) - q0 * nwarps;
+  const unsigned long long nw = erow < nwarps ? erow : nwarps;
+  unsigned long long t = 0;
+#pragma unroll 4
+  for (unsigned long long w = threadIdx.x; w < nw; w += blockDim.x)
+    t += __ldcg(&cum[w + nwarps * (w <= r0 ? q0 : q0 - 1)]);
+  return t;
 }
 
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).

@@ -27,7 +27,8 @@ struct U8Args {
   vt_result* res;
   unsigned dbg;  // debug switches (VT_DEBUG env), 0 in production
   const unsigned* skip;  // validate only: device count of leading bytes to skip, or null
-  unsigned* rows;        // validate only: per-row counts scratch (rows_utf8 entries)
+  unsigned* rows;        // validate only: per-row running totals of each warp (rows_utf8 entries)
+  unsigned long long out_cap;  // output capacity in bytes (VT_CHECKS builds check it)
 };
 
 // UTF-16 side: same conventions in units (`head` in units, 0..7).
@@ -41,7 +42,8 @@ struct U16Args {
   unsigned long long* status;
   Ctl* ctl;
   vt_result* res;
-  unsigned* rows;  // validate only: per-row counts scratch (rows_utf16 entries)
+  unsigned* rows;  // validate only: per-row running totals of each warp (rows_utf16 entries)
+  unsigned long long out_cap;  // output capacity in bytes (VT_CHECKS builds check it)
 };
 
 // launch modes: validate/count, transcode to UTF-16LE / UTF-8, transcode to
@@ -57,6 +59,7 @@ int launch_utf8(const U8Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf8(bool transcode);
 unsigned tiles_utf8(unsigned long long head, unsigned long long n);
 unsigned rows_utf8(unsigned long long head, unsigned long long n);
+
 
 int launch_utf16(const U16Args& a, int mode, int grid, cudaStream_t s);
 int occupancy_utf16(bool transcode);

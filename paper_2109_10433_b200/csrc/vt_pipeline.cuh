@@ -21,6 +21,9 @@
 // kernels in k_utf8.cu / k_utf16.cu.)
 #pragma once
 
+#include <cstddef>
+#include <cstdio>
+
 #include "vt_device.cuh"
 
 namespace vt {
@@ -42,6 +45,12 @@ namespace vt {
 // the decode; 2: right after that barrier)
 #ifndef VT_GRAB_EARLY
 #define VT_GRAB_EARLY 0
+#endif
+// skip the decode and copy-out of tiles behind an error found meanwhile (the
+// compute warps' own check: +2% on cfg2, r2h A/B, so off -- dead tiles skip
+// their copy-out through the look-back, which gives up on them at once)
+#ifndef VT_DEAD_SKIP
+#define VT_DEAD_SKIP 0
 #endif
 
 #ifndef VT_COMPUTE_THREADS
@@ -80,6 +89,7 @@ __device__ __forceinline__ void finalize_if_last(const Args& a, bool transcode,
       a.ctl->err = kNoError;
       __threadfence();
       a.ctl->done = 0;
+      VT_TR_MAX(6);
     }
   }
 }
@@ -111,16 +121,38 @@ struct PipeSmem {
   unsigned scan[kComputeThreads / 32];
   unsigned red[kComputeThreads / 32];
   unsigned tile;
+  unsigned dead;  // the tile being decoded lies behind a known error
+  unsigned long long err_now;  // thread 0's latest view of the error word
   // hand-off between the compute warps and the look-back warp (rings indexed
   // by the CTA-local tile number, guarded by the named barriers below)
   unsigned lb_tile[4], agg[2];
   unsigned long long excl[2];
 };
 
+// (vt_device.cuh's staging-store check assumes this tail size)
+struct PipeTailProbe {
+  static constexpr int kStageBytes = 16, kNStage = 1;
+};
+static_assert(offsetof(PipeSmem<PipeTailProbe>, excl) + 16 - offsetof(PipeSmem<PipeTailProbe>, scan) ==
+                  kPipeTail,
+              "PipeSmem tail");
+
 template <class C>
 __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const uint8_t* stage,
                                               unsigned long long excl, unsigned agg) {
   if (excl == ~0ull) return;  // a tile before this one failed: output is dead
+#if VT_CHECKS
+  if ((excl + agg) * C::kOutBytes > a.out_cap)
+    vt_check_fail("copy-out", excl * C::kOutBytes, (unsigned long long)agg * C::kOutBytes, 0, a.out_cap);
+  if (threadIdx.x == 0) {
+    // the staged bytes the copy-out reads lie inside the staging region
+    uint32_t dsz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+    const uint32_t s0 = smem_addr(stage), lo = smem_addr(vt_dyn_smem);
+    if (s0 + agg * C::kOutBytes > lo + dsz - kPipeTail)
+      vt_check_fail("staged tile", s0, agg * C::kOutBytes, lo, lo + dsz - kPipeTail);
+  }
+#endif
 #ifdef VT_EXP_NOCOPY
   return;
 #endif
@@ -176,6 +208,7 @@ template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
   constexpr int NS = C::kNStage;
   static_assert(NS == 1 || NS == 2, "one or two staging buffers");
+  if (threadIdx.x == 0) VT_TR_MIN(0);
   if (threadIdx.x >= kComputeThreads) {
     const bool leader = threadIdx.x == kComputeThreads;
     for (unsigned j = 0;; j++) {
@@ -199,6 +232,12 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // (the compute warps already published the aggregate, tile 0 its prefix)
       if (leader && tile != 0 && excl != ~0ull)
         store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + sm.agg[j & 1]));
+#ifdef VT_TRACE
+      if (leader) {
+        const unsigned long long e = load_relaxed(&a.ctl->err);
+        if (e != kNoError && (e + a.head) / C::kTileElems == tile) VT_TR_MAX(4);
+      }
+#endif
       if (leader) sm.excl[j & 1] = excl;
       bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
     }
@@ -246,6 +285,14 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       typename C::TileCount tc;
       unsigned off, agg;
       C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
+#ifdef VT_TRACE
+      bool tr_err_tile = false;
+      if (threadIdx.x == 0) {
+        const unsigned long long e = load_relaxed(&a.ctl->err);
+        tr_err_tile = e != kNoError && (e + a.head) / C::kTileElems == tile;
+        if (tr_err_tile) VT_TR_MAX(2);
+      }
+#endif
       if (threadIdx.x == 0) {
         // publish the aggregate right away (tile 0: the inclusive prefix), so
         // other CTAs' look-backs never wait on this CTA's look-back warp
@@ -258,10 +305,21 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       if (threadIdx.x == 0) atomicAdd(&g_phase_sub[3], (unsigned long long)ph_t);
 #endif
       unsigned grabbed = 0;
+      bool dead = false;
       const bool early = VT_GRAB_EARLY && NS == 1 && j > 0;
+      if (VT_DEAD_SKIP && threadIdx.x == 0) sm.err_now = err_seen;
       if (NS == 1 && j > 0) {
         if (early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
+        // a tile behind an error found meanwhile is dead: its output is never
+        // read, so its decode and copy-out are skipped (the load's latency
+        // hides behind the copy-out; the flag goes out with the barrier below)
+        unsigned long long e_now = 0;
+        if (VT_DEAD_SKIP && threadIdx.x == 0) e_now = load_relaxed(&a.ctl->err);
         copy_prev();
+        if (VT_DEAD_SKIP && threadIdx.x == 0) {
+          sm.err_now = e_now;
+          sm.dead = e_now != kNoError && (e_now + a.head) / C::kTileElems < tile ? 1u : 0u;
+        }
         if (early && threadIdx.x == 0) {
           unsigned t = grabbed;
           if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
@@ -271,6 +329,14 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         }
         ComputeSync::sync();  // the buffer is free (and the next tile id is out)
         VT_PH(4);
+        if (VT_DEAD_SKIP && sm.dead) agg = 0;  // (nothing staged, nothing to copy out)
+        // the look-back gave up on tile j-1: it lies behind an error, and so
+        // does tile j (taken later): its decode and copy-out are skipped (free:
+        // the offset was waited for anyway)
+        if (sm.excl[(j - 1) & 1] == ~0ull) {
+          dead = true;
+          agg = 0;
+        }
         if (early && VT_GRAB_EARLY == 2) bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
       }
       // thread 0 takes the next tile from inside the decode (the codec says
@@ -283,17 +349,23 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         if (!early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
       };
 #ifndef VT_EXP_NOEMIT
-      C::emit(a, tc, sm.out[j % NS], off, grab);
+      if (dead || (VT_DEAD_SKIP && NS == 1 && j > 0 && sm.dead))
+        grab();
+      else
+        C::emit(a, tc, sm.out[j % NS], off, grab);
 #else
       grab();
 #endif
       VT_PH(5);
+#ifdef VT_TRACE
+      if (tr_err_tile) VT_TR_MAX(3);
+#endif
       if (threadIdx.x == 0 && !early) {
         // (the error word was read at the top of the tile: one round trip
         // less on the path every warp waits for at the loop-top barrier)
         unsigned t = grabbed;
-        if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t)
-          t = a.ntiles;
+        const unsigned long long e = VT_DEAD_SKIP ? sm.err_now : err_seen;
+        if (t < a.ntiles && e != kNoError && (e + a.head) / C::kTileElems < t) t = a.ntiles;
         sm.tile = t;
         sm.lb_tile[(j + 1) & 3] = t;
       }
@@ -309,6 +381,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       j++;
     }
     if (j > 0) copy_prev();
+    if (threadIdx.x == 0) VT_TR_MAX(5);
   }
   finalize_if_last(a, true, C::kTileElems);
 }

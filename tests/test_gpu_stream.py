@@ -153,7 +153,7 @@ int main(int, char** argv) {
 }
 ''')
     exe = tmp_path / "blk"
-    libdir = os.path.dirname(vt.LIB_PATH)
+    libdir = os.path.join(os.path.dirname(vt.__file__), "lib")  # the in-tree library (not a VT_LIB variant)
     subprocess.run(["g++", "-std=c++20", "-O1", str(src), "-I", os.path.join(ROOT, "include"), "-L", libdir,
                     "-lvtrans_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe), str(blob)], capture_output=True, text=True, timeout=300).stdout.split()
