@@ -23,6 +23,7 @@
 //      into the shared-memory staging buffer.
 #include "vt_kernels.h"
 #include "vt_pipeline.cuh"
+#include "vt_swar.cuh"
 
 namespace vt {
 
@@ -215,57 +216,30 @@ struct Class16 {
   bool err;
 };
 
-// Phase A over the 16 own words: pairing check and counts (SWAR, 16-bit lanes).
-// The kernel is bound by the ALU pipe: the surrogate test is one masked XOR and
-// a carry (the add runs on the FMA pipe).  (Summing the flags with IMAD.HI
-// instead of shift + add measured slower: IMAD.HI is quarter rate.)
+// Phase A over the thread's 32 units: pairing check and counts, four units per
+// operation on the low-byte / high-byte planes of each pair of words
+// (vt_swar.cuh; the kernel is bound by the ALU pipe, and the 16-bit-lane form
+// this replaces spent twice the instructions per unit).
 __device__ __forceinline__ Class16 classify16(const Words16& W) {
-  uint32_t hp;  // high-surrogate plane of the previous word
-  {
-    const uint32_t x = W.w[0];
-    hp = sur16(x) & ~(x << 5);
-  }
-  uint32_t err = 0, acc = 0, nlo = 0, nsur = 0;
-  // (0x58005800 in an opaque register, as in the emit, measured +-0 here)
-  constexpr uint32_t K58 = 0x58005800u;
+  using namespace swar;
+  uint32_t k58 = 0x58585858u;
+  asm volatile("" : "+r"(k58));  // (a & imm) ^ k58 is one LOP3 only with k58 in a register
+  Count16 c;
+  c.err = c.acc = c.nsur = c.nlo = 0;
+  c.hp = hs_plane(hi_plane(0u, W.w[0]), k58);  // (lane 3: the unit before the range)
 #pragma unroll
-  for (int k = 1; k <= K16_WPT + 1; k++) {
-    const uint32_t x = W.w[k];
-    // (t through an asm LOP3: emit_word16_v3 has the same expression, and a
-    // shared value would stay live across the scan and spill)
-    const uint32_t t = lop3<0x6A>(x, 0x78007800u, K58);  // (a & b) ^ c: 0 on D800..DFFF
-    const uint32_t sr = lop3<0x20>(x, t + 0x78007800u, H16);  // a & ~b & c
-    const uint32_t x5 = x * 32u;                               // bit 10 (low surrogate) -> 15
-    const uint32_t hm = sr & ~x5, lm = sr & x5;
-    {
-      // pairs of consecutive units ending in word k: the unit before each unit
-      // is a high surrogate exactly when the unit is a low one.  One XOR flags
-      // both failures (a high one not followed by a low one, a low one not
-      // after a high one); pairs with a unit outside the thread's own range
-      // (w[0]'s last, w[17]'s) may flag a neighbour's error, which sends this
-      // thread through the exact check, which then finds none of its own.
-      // (2 ALU ops per word fewer than testing the two failures separately:
-      // cfg3 1.119 -> 1.081 ms.  Written in C: the same as an asm LOP3 makes
-      // ptxas 12.9 crash.)
-      const uint32_t prev_hi = __funnelshift_l(hp, hm, 16);
-      err |= prev_hi ^ lm;
-      hp = hm;
-    }
-    if (k <= K16_WPT) {
-      const uint32_t x15 = x & 0x7FFF7FFFu;
-      acc += (ge80_16(x, x15) >> 15) + (ge800_16(x, x15) >> 15);
-      nlo += lm >> 15;
-      nsur += sr >> 15;
-    }
+  for (int g = 0; g < K16_WPT / 2; g++) {
+    const uint32_t x0 = W.w[1 + 2 * g], x1 = W.w[2 + 2 * g];
+    count_group16<true>(lo_plane(x0, x1), hi_plane(x0, x1), k58, c);
   }
-  Class16 c;
-  const unsigned a = (acc & 0xFFFFu) + (acc >> 16), l = (nlo & 0xFFFFu) + (nlo >> 16);
-  const unsigned sn = (nsur & 0xFFFFu) + (nsur >> 16);
+  // the unit after the range closes the last pair
+  count_group16<false>(lo_plane(W.w[K16_WPT + 1], 0u), hi_plane(W.w[K16_WPT + 1], 0u), k58, c);
+  Class16 r;
   // bytes per unit: 1 + [u >= 0x80] + [u >= 0x800] - [surrogate] (2 + 2 per pair)
-  c.bytes = K16_UPT + a - sn;
-  c.chars = K16_UPT - l;
-  c.err = err != 0;
-  return c;
+  r.bytes = K16_UPT + lane_sum(c.acc) - lane_sum(c.nsur);
+  r.chars = K16_UPT - lane_sum(c.nlo);
+  r.err = c.err != 0;
+  return r;
 }
 
 template <bool kTranscode, int NT, class Sync, bool kBE = false>
@@ -330,114 +304,37 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   off = block_excl_scan<NT, Sync, false>(tc.cnt, scan, agg);
 }
 
-// Both units of a word at once (16-bit SWAR lanes).  Every unit is written
-// as 1-3 bytes: BMP units as themselves; a surrogate pair's 4 bytes are split
-// 2 + 2 between its halves -- with w = (hi & 0x3FF) + 0x40 (code point bits
-// 10..20), the high half writes F0|w>>8, 80|(w>>2)&3F and the low half writes
-// 80|(w&3)<<4|(lo>>6)&0xF, 80|lo&3F, where w & 3 == hi & 3.  So no lane needs
-// its neighbour except for two bits of the previous unit (px: previous word).
-// Written for few ALU-pipe instructions (the kernel is bound by the ALU pipe;
-// IMAD and IADD go to the FMA pipe):
-//  * only the low byte of each 16-bit lane has to be right (sts8 stores the
-//    low byte), so most masks after right shifts disappear;
-//  * the surrogate test is one masked XOR and a carry (no shift);
-//  * kOverlap: all three bytes of both units are stored unconditionally and q
-//    advances by the real lengths -- a unit's unused S/T bytes land where the
-//    next unit's bytes go and are overwritten by them (same thread, program
-//    order).  Only the thread's last word may not spill (the bytes after it
-//    belong to the next thread): it takes the predicated form.
-// The 2nd / 3rd byte stores of the overlapping form are predicated on the
-// unit needing them (non-ASCII / 3-byte): fewer shared-memory wavefronts for
-// one LOP3 per store (the kernel is bound by the ALU pipe and the shared-memory
-// data pipe together: ALU 79 %, L1/shared 77 %).  r2h A/B, cfg3: 1.095 ->
-// 1.080 ms (both), 1.081 (3rd byte only).
-#ifndef VT_U16_PRED_S
-#define VT_U16_PRED_S 1
+// ---- encode: four units per operation (vt_swar.cuh) -------------------------
+// encode_group16 gives the UTF-8 bytes of a group's four units as three byte
+// planes (first / second / third byte) and the planes saying which units have
+// a second and a third byte.  Every unit writes 1-3 bytes (a surrogate pair's
+// 4 bytes are split 2 + 2 between its halves, so a pair may straddle threads
+// and tiles): the first byte unconditionally, the second and third predicated
+// on the unit having them, the tests going straight into the predicates (one
+// LOP3 each) which also advance the running address.  Nothing is written
+// beyond a unit's own bytes, so no word needs a special form.
+#ifndef VT_GRAB_AT_G16
+#define VT_GRAB_AT_G16 5  // groups encoded before the next tile is taken (of 8)
 #endif
-#ifndef VT_U16_PRED_T
-#define VT_U16_PRED_T 1
-#endif
-// Byte store at a when `plane` has bit MASK set (the test goes straight into
-// the predicate, one LOP3).
 template <uint32_t MASK>
-__device__ __forceinline__ void sts8_if(uint32_t a, uint32_t v, uint32_t plane) {
-  VT_CHECK_STS(a, 1);
+__device__ __forceinline__ void store_unit16(uint32_t& q, uint32_t F, uint32_t S, uint32_t T,
+                                             uint32_t z80, uint32_t is3) {
+  if (VT_CHECKS) VT_CHECK_STS(q, 1 + ((z80 & MASK) ? 1 : 0) + ((is3 & MASK) ? 1 : 0));
   asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 d;\n\t"
-      "lop3.or.b32 d|p, %1, 0, %2, 0xA0, 0;\n\t"  // a & c
-      "@p st.shared.u8 [%0], %3;\n\t}"
-      :
-      : "r"(a), "r"(plane), "n"(MASK), "r"(v));
-}
-
-template <bool kOverlap>
-__device__ __forceinline__ void emit_word16_v3(uint32_t x, uint32_t px, uint32_t& q, uint32_t K80,
-                                               uint32_t KE0, uint32_t K58) {
-  // (x15 through an asm LOP3: classify16 computes the same compare planes, and
-  // if the compiler shares them they stay live across the scan and spill)
-  const uint32_t x15 = lop3<0xC0>(x, 0x7FFF7FFFu, 0u);
-  const uint32_t g80 = lop3<0xA8>(x15 + 0x7F807F80u, x, H16);    // u >= 0x80
-  const uint32_t g800 = lop3<0xA8>(x15 + 0x78007800u, x, H16);   // u >= 0x800
-  // D800..DFFF: bit 15 set and bits 11..14 == 1011
-  const uint32_t t = lop3<0x6A>(x, 0x78007800u, K58);            // (a & b) ^ c
-  const uint32_t sur = lop3<0x20>(x, t + 0x78007800u, H16);       // a & ~b & c
-  const uint32_t hs = sur & ~(x * 32u);                           // bit 10 clear: high
-  const uint32_t is3 = g800 & ~sur;
-  const uint32_t m80 = prmt(g80, 0, 0xBB99), m3 = prmt(is3, 0, 0xBB99);
-  const uint32_t ms = prmt(sur, 0, 0xBB99), mh = prmt(hs, 0, 0xBB99);
-  // lengths 1 + [u >= 0x80] + [3-byte BMP]: a pair's halves write 2 + 2
-  const uint32_t n = 0x00010001u + (g80 >> 15) + (is3 >> 15);
-  const uint32_t q1 = q + (n & 0xFFFFu);
-  const uint32_t x6 = x >> 6;                                     // low byte: u bits 6..13
-  // first byte: ASCII u; 2-byte C0 | u>>6 (u < 0x800: bits 11..13 are 0);
-  // 3-byte E0 | u>>12; high surrogate F0 | w>>8; low surrogate 80 | (w&3)<<4 | (u>>6)&F
-  const uint32_t w = (x & 0x03FF03FFu) + 0x00400040u;              // code point bits 10..20
-  uint32_t F1;
-  {
-    const uint32_t F2 = x6 | 0x00C000C0u;
-    const uint32_t F3 = lop3<0xEA>(x >> 12, 0x000F000Fu, KE0);      // (a & b) | c
-    const uint32_t Fh = (w >> 8) | 0x00F000F0u;
-    const uint32_t pu16 = prmt(px, x, 0x5432) * 16u;                // previous unit << 4
-    const uint32_t Fl = lop3<0xEA>(lop3<0xCA>(0x000F000Fu, x6, pu16), 0x003F003Fu, K80);
-    // selections (mux(m, a, b) = m ? a : b, LOP3 0xCA with the mask first)
-    const uint32_t Fn = lop3<0xCA>(ms, lop3<0xCA>(mh, Fh, Fl), lop3<0xCA>(m3, F3, F2));
-    const uint32_t F = lop3<0xCA>(m80, Fn, x);
-    sts8(q, F);
-    F1 = F >> 16;
-  }
-  const uint32_t T = lop3<0xEA>(x, 0x003F003Fu, K80);
-  const uint32_t S = lop3<0xEA>(lop3<0xCA>(m3, x6, lop3<0xCA>(mh, w >> 2, x)), 0x003F003Fu, K80);
-  if (kOverlap) {
-#if VT_U16_PRED_S
-    sts8_if<0x00008000u>(q + 1, S, g80);
-#else
-    sts8(q + 1, S);
-#endif
-#if VT_U16_PRED_T
-    sts8_if<0x00008000u>(q + 2, T, is3);
-#else
-    sts8(q + 2, T);
-#endif
-    sts8(q1, F1);
-#if VT_U16_PRED_S
-    sts8_if<0x80000000u>(q1 + 1, S >> 16, g80);
-#else
-    sts8(q1 + 1, S >> 16);
-#endif
-#if VT_U16_PRED_T
-    sts8_if<0x80000000u>(q1 + 2, T >> 16, is3);
-#else
-    sts8(q1 + 2, T >> 16);
-#endif
-  } else {
-    const uint32_t n0 = n & 0xFFFFu, n1 = n >> 16;
-    if (n0 >= 2) sts8(q + 1, S);
-    if (n0 == 3) sts8(q + 2, T);
-    sts8(q1, F1);
-    if (n1 >= 2) sts8(q1 + 1, S >> 16);
-    if (n1 == 3) sts8(q1 + 2, T >> 16);
-  }
-  q = q1 + (n >> 16);
+      "{\n\t.reg .pred p, r;\n\t.reg .b32 d, t;\n\t"
+      "lop3.or.b32 d|p, %4, 0, %6, 0xA0, 0;\n\t"  // a & c
+      "lop3.or.b32 d|r, %5, 0, %6, 0xA0, 0;\n\t"
+      "st.shared.u8 [%0], %1;\n\t"
+      "@p st.shared.u8 [%0+1], %2;\n\t"
+      "@r st.shared.u8 [%0+2], %3;\n\t"
+      // (three writes of t from q, the last true predicate wins: one add of
+      // latency per unit instead of a chain of three)
+      "add.u32 t, %0, 1;\n\t"
+      "@p add.u32 t, %0, 2;\n\t"
+      "@r add.u32 t, %0, 3;\n\t"
+      "mov.u32 %0, t;\n\t}"
+      : "+r"(q)
+      : "r"(F), "r"(S), "r"(T), "r"(z80), "r"(is3), "n"(MASK));
 }
 
 #ifndef VT_NSTAGE16
@@ -465,25 +362,25 @@ struct Utf16Codec {
       // (tc.lo > 0 only for the first thread of a call: the zeros before the
       // input are encoded too and land in the pad before the staging buffer)
       uint32_t q = smem_addr(stage) + off - tc.lo;
-      // constants or'ed in after a mask, in registers: LOP3 takes one
-      // immediate, so "(v & imm) | K" is one instruction only with K in a
-      // register (opaque, or ptxas folds it back into two)
-      uint32_t K80 = 0x00800080u, KE0 = 0x00E000E0u, K58 = 0x58005800u;
-      asm volatile("" : "+r"(K80), "+r"(KE0), "+r"(K58));
+      using namespace swar;
+      const K16 k = make_k16();
+      uint32_t lo_prev = lo_plane(0u, tc.W.w[0]);  // (lane 3: the unit before the range)
 #pragma unroll
-      for (int k = 1; k < K16_WPT; k++) {
-        if (k == VT_GRAB_AT_U16 + 1) {
+      for (int g = 0; g < K16_WPT / 2; g++) {
+        if (g == VT_GRAB_AT_G16) {
           mid();
           __syncwarp();  // (keeps ptxas from sinking the atomic behind the stores)
         }
-        emit_word16_v3<true>(tc.W.w[k], tc.W.w[k - 1], q, K80, KE0, K58);
+        const uint32_t x0 = tc.W.w[1 + 2 * g], x1 = tc.W.w[2 + 2 * g];
+        const uint32_t lo = lo_plane(x0, x1), hi = hi_plane(x0, x1);
+        const Enc16 e = encode_group16(lo, hi, lo_prev, k);
+        store_unit16<0x00000080u>(q, e.F, e.S, e.T, e.z80, e.is3);
+        store_unit16<0x00008000u>(q, e.F >> 8, e.S >> 8, e.T >> 8, e.z80, e.is3);
+        store_unit16<0x00800000u>(q, e.F >> 16, e.S >> 16, e.T >> 16, e.z80, e.is3);
+        store_unit16<0x80000000u>(q, e.F >> 24, e.S >> 24, e.T >> 24, e.z80, e.is3);
+        lo_prev = lo;
       }
-      if (VT_GRAB_AT_U16 == K16_WPT - 1) {
-        mid();
-        __syncwarp();
-      }
-      emit_word16_v3<false>(tc.W.w[K16_WPT], tc.W.w[K16_WPT - 1], q, K80, KE0, K58);
-      if (VT_GRAB_AT_U16 >= K16_WPT) mid();
+      if (VT_GRAB_AT_G16 >= K16_WPT / 2) mid();
     } else {
       mid();
       const Words16 tmp = tc.W;
