@@ -248,22 +248,30 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
                                              unsigned& agg) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K16_TILE;
-  tc.v0 = vt0 + (long long)K16_UPT * threadIdx.x;
-  const Src16 src{a.base, a.head, a.n, kBE};
-  const bool interior =
-      vt0 - 2 >= (long long)a.head && vt0 + K16_TILE + 2 <= (long long)(a.head + a.n);
+  // interior tiles (all but the first and the last one or two): one uniform
+  // compare, no 64-bit range arithmetic (as count_tile in k_utf8.cu)
+  const unsigned long long endv = a.head + a.n;
+  const unsigned last_in = endv >= K16_TILE + 2 ? (unsigned)((endv - 2) / K16_TILE) : 0u;
+  const bool interior = tile >= 1 && tile < last_in;
+  unsigned hi;
   if (interior) {
-    load_lane_words<K16_WPT>(reinterpret_cast<const uint8_t*>(a.base + tc.v0), lane, tc.W.w);
+    load_lane_words<K16_WPT>(reinterpret_cast<const uint8_t*>(a.base) + (size_t)tile * (2 * K16_TILE) +
+                                 (size_t)(2 * K16_UPT * threadIdx.x),
+                             lane, tc.W.w);
     if (kBE) {
 #pragma unroll
       for (int k = 0; k < K16_WPT + 2; k++) tc.W.w[k] = prmt(tc.W.w[k], 0, 0x2301);
     }
+    tc.lo = 0;
+    hi = K16_UPT;
   } else {
+    tc.v0 = vt0 + (long long)K16_UPT * threadIdx.x;
+    const Src16 src{a.base, a.head, a.n, kBE};
     load_edge16<kBE>(src, tc.v0, tc.W.w);
+    const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
+    tc.lo = (unsigned)max(0LL, min((long long)K16_UPT, s));
+    hi = (unsigned)max((long long)tc.lo, min((long long)K16_UPT, e));
   }
-  const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
-  tc.lo = (unsigned)max(0LL, min((long long)K16_UPT, s));
-  const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K16_UPT, e));
   tc.lim = hi;
   const Class16 c = classify16(tc.W);
   unsigned my_err = kNone16;
@@ -364,7 +372,6 @@ struct Utf16Codec {
       uint32_t q = smem_addr(stage) + off - tc.lo;
       using namespace swar;
       const K16 k = make_k16();
-      uint32_t lo_prev = lo_plane(0u, tc.W.w[0]);  // (lane 3: the unit before the range)
 #pragma unroll
       for (int g = 0; g < K16_WPT / 2; g++) {
         if (g == VT_GRAB_AT_G16) {
@@ -373,12 +380,11 @@ struct Utf16Codec {
         }
         const uint32_t x0 = tc.W.w[1 + 2 * g], x1 = tc.W.w[2 + 2 * g];
         const uint32_t lo = lo_plane(x0, x1), hi = hi_plane(x0, x1);
-        const Enc16 e = encode_group16(lo, hi, lo_prev, k);
+        const Enc16 e = encode_group16(lo, hi, tc.W.w[2 * g], k);
         store_unit16<0x00000080u>(q, e.F, e.S, e.T, e.z80, e.is3);
         store_unit16<0x00008000u>(q, e.F >> 8, e.S >> 8, e.T >> 8, e.z80, e.is3);
         store_unit16<0x00800000u>(q, e.F >> 16, e.S >> 16, e.T >> 16, e.z80, e.is3);
         store_unit16<0x80000000u>(q, e.F >> 24, e.S >> 24, e.T >> 24, e.z80, e.is3);
-        lo_prev = lo;
       }
       if (VT_GRAB_AT_G16 >= K16_WPT / 2) mid();
     } else {

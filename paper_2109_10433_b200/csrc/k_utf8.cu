@@ -542,15 +542,26 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
                                            unsigned& agg) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K8_TILE;  // virtual start of the tile
-  tc.v0 = vt0 + (long long)K8_BPT * threadIdx.x;
-  const Src src{a.base, a.head, a.n};
-  // interior: the tile and both halo words lie inside the input
-  const bool interior =
-      vt0 - 4 >= (long long)a.head && vt0 + K8_TILE + 4 <= (long long)(a.head + a.n);
+  // interior: the tile and both halo words lie inside the input.  head < 16, so
+  // every tile but the first starts past it; `last_in` is uniform (kernel
+  // parameters only), so the test is one compare per tile and the interior
+  // path carries no 64-bit range arithmetic (it was ~50 instructions per tile
+  // and thread).
+  const unsigned long long endv = a.head + a.n;
+  const unsigned last_in = endv >= K8_TILE + 4 ? (unsigned)((endv - 4) / K8_TILE) : 0u;  // tiles [1, last_in) are interior
+  const bool interior = tile >= 1 && tile < last_in;
+  unsigned hi;
   if (interior) {
-    load_lane_words<K8_WPT>(a.base + tc.v0, lane, tc.W.w);
+    load_lane_words<K8_WPT>(a.base + (size_t)tile * K8_TILE + (size_t)(K8_BPT * threadIdx.x), lane, tc.W.w);
+    tc.lo = 0;
+    hi = K8_BPT;
   } else {
+    tc.v0 = vt0 + (long long)K8_BPT * threadIdx.x;
+    const Src src{a.base, a.head, a.n};
     load_edge(src, tc.v0, tc.W.w);
+    const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
+    tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
+    hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
   }
 #ifdef VT_PHASES
   {  // sub-phase probe: wait for the loads
@@ -562,9 +573,6 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     if (threadIdx.x == 0) atomicAdd(&g_phase_sub[0], (unsigned long long)t);
   }
 #endif
-  const long long s = (long long)a.head - tc.v0, e = (long long)(a.head + a.n) - tc.v0;
-  tc.lo = (unsigned)max(0LL, min((long long)K8_BPT, s));
-  const unsigned hi = (unsigned)max((long long)tc.lo, min((long long)K8_BPT, e));
   const ClassOut co = kNV ? classify_nv(tc.W) : classify(tc.W);
 #ifdef VT_PHASES
   {

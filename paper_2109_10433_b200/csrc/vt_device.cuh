@@ -339,27 +339,48 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
 // WS..WS+4 of the two aligned 16-byte source chunks starting at 16(c-1) (+16
 // for mis == 0), then a byte funnel shift.  WS and the shift are the same for
 // every chunk, so the loop is instantiated per WS.
-template <int WS>
+template <int WS, bool kShift>
+__device__ __forceinline__ void copy_chunk(uint8_t* __restrict__ d, uint32_t a, unsigned bs) {
+  uint32_t x[8];
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(a + 16));
+  uint4 v;
+  if (kShift) {
+    v.x = __funnelshift_r(x[WS], x[WS + 1], bs);
+    v.y = __funnelshift_r(x[WS + 1], x[WS + 2], bs);
+    v.z = __funnelshift_r(x[WS + 2], x[WS + 3], bs);
+    v.w = __funnelshift_r(x[WS + 3], x[WS + 4], bs);
+  } else {  // source and destination congruent mod 4: whole words
+    v.x = x[WS];
+    v.y = x[WS + 1];
+    v.z = x[WS + 2];
+    v.w = x[WS + 3];
+  }
+  *reinterpret_cast<uint4*>(d) = v;
+}
+
+template <int WS, bool kShift>
 __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_t sbase,
                                             unsigned mis, unsigned len, unsigned bs,
                                             unsigned nthreads) {
   const unsigned end = mis + len;
   const unsigned c_end = end >> 4;  // chunks [mis ? 1 : 0, c_end) are whole
-  // whole chunks: two independent iterations per step (more stores in flight)
+  // whole chunks: running addresses with constant strides, two independent
+  // chunks per step (more stores in flight)
+  const unsigned c0 = (mis ? 1u : 0u) + threadIdx.x;
+  if (c0 < c_end) {
+    unsigned n = (c_end - c0 + nthreads - 1) / nthreads;
+    uint32_t a = sbase + 16u * c0 - (mis ? 16u : 0u);
+    uint8_t* d = dbase + 16u * c0;
+    const unsigned step = 16u * nthreads;
 #pragma unroll 2
-  for (unsigned c = (mis ? 1u : 0u) + threadIdx.x; c < c_end; c += nthreads) {
-    const uint32_t a = sbase + 16u * c - (mis ? 16u : 0u);
-    uint32_t x[8];
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(a));
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(a + 16));
-    uint4 v;
-    v.x = __funnelshift_r(x[WS], x[WS + 1], bs);
-    v.y = __funnelshift_r(x[WS + 1], x[WS + 2], bs);
-    v.z = __funnelshift_r(x[WS + 2], x[WS + 3], bs);
-    v.w = __funnelshift_r(x[WS + 3], x[WS + 4], bs);
-    *reinterpret_cast<uint4*>(dbase + 16 * c) = v;
+    for (; n; n--) {
+      copy_chunk<WS, kShift>(d, a, bs);
+      a += step;
+      d += step;
+    }
   }
   // the partial first chunk (bytes [mis, 16)) and last chunk (bytes
   // [16 c_end, end)): one byte per thread, threads 0..15 and 16..31
@@ -384,11 +405,17 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   const uint32_t sbase = smem_addr(src);
   const unsigned rel = (16u - mis) & 15u;  // (16c - mis) mod 16
   const unsigned bs = (rel & 3u) * 8u;
-  switch (rel >> 2) {
-    case 0: copy_out_ws<0>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 1: copy_out_ws<1>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 2: copy_out_ws<2>(dbase, sbase, mis, len, bs, nthreads); break;
-    default: copy_out_ws<3>(dbase, sbase, mis, len, bs, nthreads); break;
+  // (bs == 0 for every other tile of 2-byte output: those copy whole words
+  // without the four funnel shifts per chunk)
+  switch ((rel >> 2) | (bs ? 4u : 0u)) {
+    case 0: copy_out_ws<0, false>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 1: copy_out_ws<1, false>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 2: copy_out_ws<2, false>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 3: copy_out_ws<3, false>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 4: copy_out_ws<0, true>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 5: copy_out_ws<1, true>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 6: copy_out_ws<2, true>(dbase, sbase, mis, len, bs, nthreads); break;
+    default: copy_out_ws<3, true>(dbase, sbase, mis, len, bs, nthreads); break;
   }
 }
 

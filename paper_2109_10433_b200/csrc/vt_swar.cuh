@@ -77,13 +77,13 @@ constexpr uint32_t H8 = 0x80808080u;
 // Constants that follow a masked value into a LOP3 ("(v & imm) | K" is one
 // instruction only when K sits in a register: LOP3 takes one immediate).
 struct K16 {
-  uint32_t k80, kE0, kF0, k58;
+  uint32_t k80, kE0, k58;
 };
 VT_SWAR_FN K16 make_k16() {
-  K16 k{0x80808080u, 0xE0E0E0E0u, 0xF0F0F0F0u, 0x58585858u};
+  K16 k{0x80808080u, 0xE0E0E0E0u, 0x58585858u};
 #if defined(__CUDA_ARCH__)
   // opaque to ptxas, or it folds them back into two instructions per use
-  asm volatile("" : "+r"(k.k80), "+r"(k.kE0), "+r"(k.kF0), "+r"(k.k58));
+  asm volatile("" : "+r"(k.k80), "+r"(k.kE0), "+r"(k.k58));
 #endif
   return k;
 }
@@ -161,13 +161,13 @@ VT_SWAR_FN unsigned lane_sum(uint32_t v) { return (v * 0x01010101u) >> 24; }
 // with w = (hi & 0x3FF) + 0x40 (code point bits 10..20) the high half writes
 // F0 | w>>8, 80 | (w>>2 & 3F) and the low half 80 | (w&3)<<4 | (lo>>6 & F),
 // 80 | lo & 3F, where w & 3 == hi & 3 -- so a low surrogate needs only two
-// bits of the unit before it (`lo_prev`: the low-byte plane of the previous
-// group, whose lane 3 is that unit for lane 0).
+// bits of the unit before it (`w_prev`: the word before the group, whose upper
+// unit that is for lane 0).
 struct Enc16 {
   uint32_t F, S, T, z80, is3;
 };
 
-VT_SWAR_FN Enc16 encode_group16(uint32_t lo, uint32_t hi, uint32_t lo_prev, const K16& k) {
+VT_SWAR_FN Enc16 encode_group16(uint32_t lo, uint32_t hi, uint32_t w_prev, const K16& k) {
   Enc16 e;
   const uint32_t h7 = hi & 0x7F7F7F7Fu;
   e.z80 = l3<0xFE>(h7 + 0x7F7F7F7Fu, hi, lo);  // bit 7: u >= 0x80
@@ -186,10 +186,11 @@ VT_SWAR_FN Enc16 encode_group16(uint32_t lo, uint32_t hi, uint32_t lo_prev, cons
   const uint32_t M0 = l3<0xEA>(M, 0x0F0F0F0Fu, k.k80);        // 80 | bits 6..9
   // w >> 6 = (bits 6..9 of the unit) + 1: adding 0x40 to the low 10 bits adds
   // 1 to bits 6 and up whatever the low 6 bits are.  (Bit 7 of M0 rides along
-  // and is masked wherever W6 is used.)
-  const uint32_t W6 = M0 + 0x01010101u;
-  const uint32_t Fh = l3<0xEA>(W6 >> 2, 0x07070707u, k.kF0);
-  const uint32_t PL = pr(lo_prev, lo, 0x6543);  // lane i: low byte of unit i-1
+  // and is masked wherever W6 is used; the 0x40 added on top lands on bit 4
+  // after the shift, the 0x10 that turns E0 into the F0 of a 4-byte lead.)
+  const uint32_t W6 = M0 + 0x41414141u;
+  const uint32_t Fh = l3<0xEA>(W6 >> 2, 0x17171717u, k.kE0);
+  const uint32_t PL = pr(w_prev, lo, 0x6542);  // lane i: low byte of unit i-1
   const uint32_t Fl = l3<0xEA>(PL << 4, 0x30303030u, M0);
   // (mux(m, a, b) = m ? a : b is LOP3 0xCA with the mask first)
   const uint32_t Fn = l3<0xCA>(ms, l3<0xCA>(mh, Fh, Fl), l3<0xCA>(m3, F3, F2));

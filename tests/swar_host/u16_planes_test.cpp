@@ -74,17 +74,17 @@ static std::vector<uint16_t> valid_stream(size_t n, int mode) {
 // kernel does; `prev` is the unit before s[0]
 static void planes_encode(const uint16_t* s, size_t n, unsigned prev, std::vector<uint8_t>& out) {
   const K16 k = make_k16();
-  uint32_t lo_prev = (uint32_t)(prev & 0xFF) << 24;
+  uint32_t w_prev = (uint32_t)prev << 16;
   for (size_t g = 0; g < n; g += 4) {
     const uint32_t x0 = s[g] | ((uint32_t)s[g + 1] << 16), x1 = s[g + 2] | ((uint32_t)s[g + 3] << 16);
     const uint32_t lo = lo_plane(x0, x1), hi = hi_plane(x0, x1);
-    const Enc16 e = encode_group16(lo, hi, lo_prev, k);
+    const Enc16 e = encode_group16(lo, hi, w_prev, k);
     for (int i = 0; i < 4; i++) {
       out.push_back((e.F >> (8 * i)) & 0xFF);
       if ((e.z80 >> (8 * i)) & 0x80) out.push_back((e.S >> (8 * i)) & 0xFF);
       if ((e.is3 >> (8 * i)) & 0x80) out.push_back((e.T >> (8 * i)) & 0xFF);
     }
-    lo_prev = lo;
+    w_prev = x1;
   }
 }
 
