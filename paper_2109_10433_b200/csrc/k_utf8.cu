@@ -407,6 +407,9 @@ __device__ __forceinline__ void sts16_if_lead(uint32_t& q, uint32_t c, uint32_t 
 #ifndef VT_STS4
 #define VT_STS4 0
 #endif
+#ifndef VT_R2P
+#define VT_R2P 1
+#endif
 __device__ __forceinline__ void sts16x4_if_lead(uint32_t& q, uint32_t c, uint32_t c2, uint32_t u01,
                                                 uint32_t u23) {
   if (VT_CHECKS) VT_CHECK_STS(q, 2 * __popc((~c | c2) & 0x80808080u));
@@ -453,7 +456,21 @@ __device__ __forceinline__ void emit_word(uint32_t c, uint32_t n, uint32_t& q) {
   const uint32_t u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
   // lane i starts a character: (~c | c2) bit 8i+7, tested straight into the
   // store predicate (one 3-input LOP3 per lane, no lead plane)
-#if VT_STS4
+#if VT_R2P
+  {
+    // the four lead tests as one register-to-predicate move: the clean lead
+    // plane (bit 7 of each lane), gathered into bits 1..4 by the high half of
+    // one multiply (FMA pipe; the lane bits land on distinct product bits, so
+    // no carries), then R2P -- 2 ALU-pipe instructions instead of 4
+    const uint32_t lead7 = lop3<0x8A>(c, c2, H);  // (~a | b) & c
+    // (bits 1..4: ptxas keeps P0 out of R2P and would test bit 0 separately)
+    const uint32_t m = __umulhi(lead7, 0x04081020u);
+    if (m & 2u) { sts16(q, u01); q += 2; }
+    if (m & 4u) { sts16(q, u01 >> 16); q += 2; }
+    if (m & 8u) { sts16(q, u23); q += 2; }
+    if (m & 16u) { sts16(q, u23 >> 16); q += 2; }
+  }
+#elif VT_STS4
   sts16x4_if_lead(q, c, c2, u01, u23);
 #else
   sts16_if_lead<0x00000080u>(q, c, c2, u01);
@@ -511,10 +528,18 @@ __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t&
   // (kMasked: only characters starting in the lanes `range` selects -- the
   // valid prefix of a tile with an error, the input part of an end tile)
   const uint32_t st7 = (kNV ? lead7 | (ls7 & c & ~c2) : lead7 | ls7) & (kMasked ? range : ~0u);
+#if VT_R2P
+  const uint32_t m = __umulhi(st7, 0x04081020u);  // lanes -> bits 1..4, one R2P (see emit_word)
+  if (m & 2u) { sts16(q, u01); q += 2; }
+  if (m & 4u) { sts16(q, (u01 >> 16)); q += 2; }
+  if (m & 8u) { sts16(q, u23); q += 2; }
+  if (m & 16u) { sts16(q, (u23 >> 16)); q += 2; }
+#else
   if (st7 & 0x00000080u) { sts16(q, u01); q += 2; }
   if (st7 & 0x00008000u) { sts16(q, (u01 >> 16)); q += 2; }
   if (st7 & 0x00800000u) { sts16(q, u23); q += 2; }
   if (st7 & 0x80000000u) { sts16(q, (u23 >> 16)); q += 2; }
+#endif
 }
 
 // The low surrogate of a 4-byte character whose lead is the thread's last
