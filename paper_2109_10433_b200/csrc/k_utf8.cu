@@ -507,8 +507,10 @@ __device__ __forceinline__ void emit_word_four(uint32_t c, uint32_t n, uint32_t&
   const uint32_t B = (n2 & m3) | (n1 & ~m3);
   const uint32_t lom = lop3<0xE2>(B, 0x3F3F3F3Fu, A << 6);       // (a & b) | (c & ~b)
   const uint32_t lo = (c & ~mna) | (lom & mna);
-  const uint32_t him = (((A >> 2) & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3)) & mna;
-  const uint32_t hi_ls = lop3<0xEA>(n1 >> 2, 0x03030303u, KDC);  // (a & b) | c
+  const uint32_t A2 = A >> 2;
+  const uint32_t him = ((A2 & 0x0F0F0F0Fu) | ((c << 4) & 0xF0F0F0F0u & m3)) & mna;
+  // (an ls lane is an m3 lane, so A is n1 there: the shift is shared)
+  const uint32_t hi_ls = lop3<0xEA>(A2, 0x03030303u, KDC);  // (a & b) | c
   const uint32_t hi = lop3<0xCA>(mls, hi_ls, him);
   uint32_t u01 = prmt(lo, hi, kBE ? 0x1504 : 0x5140), u23 = prmt(lo, hi, kBE ? 0x3726 : 0x7362);
   // 4-byte leads: high surrogate = 0xD7C0 + (cp >> 10)
