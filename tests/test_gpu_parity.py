@@ -308,6 +308,15 @@ def _threads():
     return max(2, min(64, os.cpu_count() or 2))
 
 
+def _reference():
+    """The unmodified reference library compiled out of tree (oracle/_ref), when
+    the build travelled with the snapshot: the full-size checks then compare
+    with the reference itself, not only with its restatement."""
+    from oracle_lib import Reference
+
+    return Reference() if Reference.available() else None
+
+
 @pytest.mark.parametrize("cfg,size", [(1, 16 << 20), (2, 1 << 30), (4, 1 << 30)])
 def test_config_utf8_full_size(cfg, size, oracle, torch):
     d_in, n, first_bad = vt.generate(cfg, size)
@@ -319,6 +328,11 @@ def test_config_utf8_full_size(cfg, size, oracle, torch):
     assert _same(r, want)
     got = d_out[: r.written].cpu().numpy().view(np.uint16)
     assert np.array_equal(got, want_out)
+    ref = _reference()
+    if ref is not None:  # the reference's own SIMD path on the same bytes
+        ref_out, ref_res = ref.utf8_to_utf16(host, threads=_threads())
+        assert _same(r, ref_res)
+        assert np.array_equal(got, ref_out)
     if cfg == 4:
         assert want.error_at == first_bad  # the generator's first injection
         v = vt.validate_utf8_device(d_in, n)
@@ -336,14 +350,30 @@ def test_config3_utf16_full_size(oracle, torch):
     host = d_in[:n].cpu().numpy().view(np.uint16)
     want_out, want = oracle.utf16_to_utf8(host, threads=_threads())
     assert _same(r, want) and want.error_at is None
-    assert np.array_equal(d_out[: r.written].cpu().numpy(), want_out)
+    got = d_out[: r.written].cpu().numpy()
+    assert np.array_equal(got, want_out)
+    ref = _reference()
+    if ref is not None:
+        ref_out, ref_res = ref.utf16_to_utf8(host, threads=_threads())
+        assert _same(r, ref_res)
+        assert np.array_equal(got, ref_out)
     v = vt.validate_utf16_device(d_in, n)
     assert v.error_at is None and v.written == oracle.count_utf16(host)
 
 
-def test_config5_round_trip_4gib(torch):
+def _char_start(host, p):
+    while p < len(host) and (int(host[p]) & 0xC0) == 0x80:
+        p += 1
+    return p
+
+
+def test_config5_round_trip_4gib(oracle, torch):
     """cfg 5 on one GPU: 4 GiB of UTF-8 -> UTF-16 -> UTF-8 must reproduce the
-    input byte for byte (size-independent property at the full shard size)."""
+    input byte for byte (size-independent property at the full shard size).
+    Each leg's output is also compared with the oracle on the first 512 MiB
+    and the last 256 MiB of the stream (transcoding valid text is prefix- and
+    suffix-stable at character boundaries), so a mistake made symmetrically
+    in both legs cannot cancel."""
     d_in, n, _ = vt.generate(5, 4 << 30)
     d16 = torch.empty(n + 8, dtype=torch.int16, device="cuda")
     r1 = vt.utf8_to_utf16_device(d_in, n, d16)
@@ -356,6 +386,28 @@ def test_config5_round_trip_4gib(torch):
     c8 = vt.validate_utf8_device(d_in, n).written
     c16 = vt.validate_utf16_device(d16, r1.written).written
     assert c8 == c16
+    # leg 1 against the oracle: head and tail of the 4 GiB stream
+    t = _threads()
+    head = d_in[: (512 << 20) + 4].cpu().numpy()
+    m = 512 << 20
+    while (int(head[m]) & 0xC0) == 0x80:
+        m -= 1
+    want16, w = oracle.utf8_to_utf16(head[:m], threads=t)
+    assert w.error_at is None
+    assert np.array_equal(d16[: w.written].cpu().numpy().view(np.uint16), want16)
+    # leg 2 on the same head: these units back to exactly these bytes
+    want8, w2 = oracle.utf16_to_utf8(want16, threads=t)
+    assert w2.error_at is None and w2.written == m
+    assert np.array_equal(d8[:m].cpu().numpy(), want8)
+    tail0 = n - (256 << 20)
+    tail = d_in[tail0:n].cpu().numpy()
+    s0 = _char_start(tail, 0)
+    want16t, wt = oracle.utf8_to_utf16(tail[s0:], threads=t)
+    assert wt.error_at is None
+    got16t = d16[r1.written - wt.written : r1.written].cpu().numpy().view(np.uint16)
+    assert np.array_equal(got16t, want16t)
+    want8t, wt2 = oracle.utf16_to_utf8(want16t, threads=t)
+    assert np.array_equal(d8[n - wt2.written : n].cpu().numpy(), want8t)
 
 
 def test_sharder_single_process(oracle):
