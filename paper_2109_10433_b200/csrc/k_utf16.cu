@@ -324,25 +324,24 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
 #ifndef VT_GRAB_AT_G16
 #define VT_GRAB_AT_G16 5  // groups encoded before the next tile is taken (of 8)
 #endif
-template <uint32_t MASK>
+// (unit I of its group: the unconditional byte per unit sits in the immediate
+// offsets, the running address takes only the predicated increments -- two
+// adds per unit -- and moves on by 4 once per group)
+template <uint32_t MASK, int I>
 __device__ __forceinline__ void store_unit16(uint32_t& q, uint32_t F, uint32_t S, uint32_t T,
                                              uint32_t z80, uint32_t is3) {
-  if (VT_CHECKS) VT_CHECK_STS(q, 1 + ((z80 & MASK) ? 1 : 0) + ((is3 & MASK) ? 1 : 0));
+  if (VT_CHECKS) VT_CHECK_STS(q + I, 1 + ((z80 & MASK) ? 1 : 0) + ((is3 & MASK) ? 1 : 0));
   asm volatile(
-      "{\n\t.reg .pred p, r;\n\t.reg .b32 d, t;\n\t"
+      "{\n\t.reg .pred p, r;\n\t.reg .b32 d;\n\t"
       "lop3.or.b32 d|p, %4, 0, %6, 0xA0, 0;\n\t"  // a & c
       "lop3.or.b32 d|r, %5, 0, %6, 0xA0, 0;\n\t"
-      "st.shared.u8 [%0], %1;\n\t"
-      "@p st.shared.u8 [%0+1], %2;\n\t"
-      "@r st.shared.u8 [%0+2], %3;\n\t"
-      // (three writes of t from q, the last true predicate wins: one add of
-      // latency per unit instead of a chain of three)
-      "add.u32 t, %0, 1;\n\t"
-      "@p add.u32 t, %0, 2;\n\t"
-      "@r add.u32 t, %0, 3;\n\t"
-      "mov.u32 %0, t;\n\t}"
+      "st.shared.u8 [%0+%7], %1;\n\t"
+      "@p st.shared.u8 [%0+%8], %2;\n\t"
+      "@r st.shared.u8 [%0+%9], %3;\n\t"
+      "@p add.u32 %0, %0, 1;\n\t"
+      "@r add.u32 %0, %0, 1;\n\t}"
       : "+r"(q)
-      : "r"(F), "r"(S), "r"(T), "r"(z80), "r"(is3), "n"(MASK));
+      : "r"(F), "r"(S), "r"(T), "r"(z80), "r"(is3), "n"(MASK), "n"(I), "n"(I + 1), "n"(I + 2));
 }
 
 #ifndef VT_NSTAGE16
@@ -381,10 +380,11 @@ struct Utf16Codec {
         const uint32_t x0 = tc.W.w[1 + 2 * g], x1 = tc.W.w[2 + 2 * g];
         const uint32_t lo = lo_plane(x0, x1), hi = hi_plane(x0, x1);
         const Enc16 e = encode_group16(lo, hi, tc.W.w[2 * g], k);
-        store_unit16<0x00000080u>(q, e.F, e.S, e.T, e.z80, e.is3);
-        store_unit16<0x00008000u>(q, e.F >> 8, e.S >> 8, e.T >> 8, e.z80, e.is3);
-        store_unit16<0x00800000u>(q, e.F >> 16, e.S >> 16, e.T >> 16, e.z80, e.is3);
-        store_unit16<0x80000000u>(q, e.F >> 24, e.S >> 24, e.T >> 24, e.z80, e.is3);
+        store_unit16<0x00000080u, 0>(q, e.F, e.S, e.T, e.z80, e.is3);
+        store_unit16<0x00008000u, 1>(q, e.F >> 8, e.S >> 8, e.T >> 8, e.z80, e.is3);
+        store_unit16<0x00800000u, 2>(q, e.F >> 16, e.S >> 16, e.T >> 16, e.z80, e.is3);
+        store_unit16<0x80000000u, 3>(q, e.F >> 24, e.S >> 24, e.T >> 24, e.z80, e.is3);
+        q += 4;
       }
       if (VT_GRAB_AT_G16 >= K16_WPT / 2) mid();
     } else {

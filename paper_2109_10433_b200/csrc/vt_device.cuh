@@ -16,7 +16,6 @@
 
 #include <cstdint>
 #include <cstdio>
-#include <cuda/atomic>
 
 #include "../../include/vtrans_gpu.h"
 
@@ -161,14 +160,18 @@ __device__ __forceinline__ unsigned long long pack_status(unsigned long long fla
   return flag | ((unsigned long long)(epoch & 0x3FFF) << 48) | (v & kValMask);
 }
 
+// Relaxed device-scope accesses to global words as plain PTX (the libcu++
+// atomic_ref forms compiled to generic-address loads behind a dispatch: ncu
+// counted ~3 % of the kernel's instructions in them, all on the look-back warp
+// and thread 0).
 __device__ __forceinline__ void store_status(unsigned long long* p, unsigned long long s) {
-  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
-  a.store(s, cuda::memory_order_relaxed);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(s) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long load_status(unsigned long long* p) {
-  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
-  return a.load(cuda::memory_order_relaxed);
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Relaxed fetch-and-increment whose position among the (volatile) shared
@@ -185,8 +188,7 @@ __device__ __forceinline__ void atom_inc_pinned(unsigned* p, bool pred, unsigned
 }
 
 __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p) {
-  cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(*p);
-  return a.load(cuda::memory_order_relaxed);
+  return load_status(p);
 }
 
 // Warp-cooperative decoupled look-back for tile `tile` (> 0), executed by one
@@ -513,6 +515,18 @@ __device__ __forceinline__ unsigned long long prefix_rows(const unsigned* cum, u
   return t;
 }
 
+// One step of a warp inclusive scan: x += (lane - o)'s x, when that lane exists
+// (the shuffle's own in-range predicate guards the add: no compare per step).
+__device__ __forceinline__ unsigned scan_step_up(unsigned x, int o) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 y;\n\t"
+      "shfl.sync.up.b32 y|p, %0, %1, 0, 0xffffffff;\n\t"
+      "@p add.u32 %0, %0, y;\n\t}"
+      : "+r"(x)
+      : "r"(o));
+  return x;
+}
+
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).
 // kTrailing: end with a barrier so warp_sums can be reused at once; callers
 // that pass a barrier before the next scan anyway can drop it.
@@ -522,10 +536,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* warp_s
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned x = v;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= (unsigned)o) x += y;
-  }
+  for (int o = 1; o < 32; o <<= 1) x = scan_step_up(x, o);
   if (lane == 31) warp_sums[wid] = x;
   Sync::sync();
   if (wid == 0) {
