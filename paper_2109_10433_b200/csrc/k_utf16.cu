@@ -417,12 +417,14 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
   // top of every row and tested at the top of the next one, so the check adds
   // no latency and a warp runs at most one row past a found error.
   unsigned long long e_prev = kNoError;
+  // rows [1, last_in) lie inside the input together with both halo words (head < 8 units)
+  const unsigned long long last_in = end >= K16_ROW + 2 ? (unsigned long long)(end - 2) / K16_ROW : 0ull;
   for (unsigned long long row = gw; row < nrows; row += nwarps) {
     const long long r0 = (long long)row * K16_ROW;
     if (e_prev != kNoError && (long long)e_prev + head < r0) break;
     const unsigned long long e_next = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
     const long long v0 = r0 + (long long)K16_UPT * lane;
-    const bool interior = r0 - 2 >= head && r0 + K16_ROW + 2 <= end;
+    const bool interior = row >= 1 && row < last_in;  // (one uniform compare, as count_tile16)
     Words16 W;
     if (interior) {
       load_lane_words<K16_WPT>(reinterpret_cast<const uint8_t*>(a.base + v0), lane, W.w);
@@ -436,9 +438,13 @@ __global__ void __launch_bounds__(256, 4) utf16_validate_rows_kernel(U16Args a) 
     const Class16 c = classify16(W);
     unsigned cnt;
     if (!c.err) {
-      const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
-      const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
-      cnt = (kUnits ? c.bytes : c.chars) - (K16_UPT - (hi - lo));  // minus the zeros outside
+      if (interior) {
+        cnt = kUnits ? c.bytes : c.chars;
+      } else {
+        const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
+        const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));
+        cnt = (kUnits ? c.bytes : c.chars) - (K16_UPT - (hi - lo));  // minus the zeros outside
+      }
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K16_UPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K16_UPT, end - v0));

@@ -768,12 +768,16 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
   // top of every row and tested at the top of the next one, so the check adds
   // no latency and a warp runs at most one row past a found error.
   unsigned long long e_prev = kNoError;
+  // rows [1, last_in) lie inside the input together with both halo words (head < 16)
+  const unsigned long long last_in = end >= K8_ROW + 4 ? (unsigned long long)(end - 4) / K8_ROW : 0ull;
   for (unsigned long long row = gw; row < nrows; row += nwarps) {
     const long long r0 = (long long)row * K8_ROW;
     if (e_prev != kNoError && (long long)e_prev + head < r0) break;
     const unsigned long long e_next = lane == 0 ? load_relaxed(&a.ctl->err) : 0ull;
     const long long v0 = r0 + (long long)K8_BPT * lane;
-    const bool interior = r0 - 4 >= head && r0 + K8_ROW + 4 <= end;
+    // interior rows (all but the first and the last one or two): one uniform
+    // compare, no 64-bit range arithmetic (as count_tile)
+    const bool interior = row >= 1 && row < last_in;
     Words W;
     if (interior) {
       load_lane_words<K8_WPT>(a.base + v0, lane, W.w);
@@ -783,9 +787,13 @@ __global__ void __launch_bounds__(256, 4) utf8_validate_rows_kernel(U8Args a) {
     const ClassOut co = classify(W);
     unsigned cnt;
     if (!co.viol) {
-      const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
-      const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
-      cnt = (kUnits ? co.units : co.chars) - (K8_BPT - (hi - lo));  // minus the zeros outside
+      if (interior) {
+        cnt = kUnits ? co.units : co.chars;
+      } else {
+        const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
+        const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
+        cnt = (kUnits ? co.units : co.chars) - (K8_BPT - (hi - lo));  // minus the zeros outside
+      }
     } else {
       const unsigned lo = (unsigned)max(0LL, min((long long)K8_BPT, head - v0));
       const unsigned hi = (unsigned)max((long long)lo, min((long long)K8_BPT, end - v0));
