@@ -217,7 +217,7 @@ __device__ __forceinline__ unsigned long long load_relaxed(unsigned long long* p
 #define VT_LB_HELP 0
 #endif
 #ifndef VT_LB_DELAY
-#define VT_LB_DELAY 3000  // ns before the first poll
+#define VT_LB_DELAY 2000  // ns before the first poll (3000 before the look-back warp took over the copy-out)
 #endif
 #ifndef VT_LB_SLEEP
 #define VT_LB_SLEEP 2000  // ns between polls of a window that is not ready
@@ -363,21 +363,25 @@ __device__ __forceinline__ void copy_chunk(uint8_t* __restrict__ d, uint32_t a, 
   *reinterpret_cast<uint4*>(d) = v;
 }
 
+#ifndef VT_COPY_UNROLL
+#define VT_COPY_UNROLL 4  // chunks in flight per thread in the copy-out loop (2: +0.6 % on cfg2, r2z)
+#endif
 template <int WS, bool kShift>
 __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_t sbase,
                                             unsigned mis, unsigned len, unsigned bs,
-                                            unsigned nthreads) {
+                                            unsigned nthreads, unsigned tid) {
   const unsigned end = mis + len;
   const unsigned c_end = end >> 4;  // chunks [mis ? 1 : 0, c_end) are whole
   // whole chunks: running addresses with constant strides, two independent
   // chunks per step (more stores in flight)
-  const unsigned c0 = (mis ? 1u : 0u) + threadIdx.x;
+  const unsigned c0 = (mis ? 1u : 0u) + tid;
   if (c0 < c_end) {
     unsigned n = (c_end - c0 + nthreads - 1) / nthreads;
     uint32_t a = sbase + 16u * c0 - (mis ? 16u : 0u);
     uint8_t* d = dbase + 16u * c0;
     const unsigned step = 16u * nthreads;
-#pragma unroll 2
+    constexpr int kCopyUnroll = VT_COPY_UNROLL;
+#pragma unroll kCopyUnroll
     for (; n; n--) {
       copy_chunk<WS, kShift>(d, a, bs);
       a += step;
@@ -386,7 +390,7 @@ __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_
   }
   // the partial first chunk (bytes [mis, 16)) and last chunk (bytes
   // [16 c_end, end)): one byte per thread, threads 0..15 and 16..31
-  const unsigned t = threadIdx.x;
+  const unsigned t = tid;
   if (t < 32) {
     const unsigned pos = t < 16 ? t : 16u * c_end + (t - 16);
     const bool first = t < 16 && mis != 0;
@@ -400,7 +404,7 @@ __device__ __forceinline__ void copy_out_ws(uint8_t* __restrict__ dbase, uint32_
 }
 
 __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_t* src,
-                                         unsigned len, unsigned nthreads) {
+                                         unsigned len, unsigned nthreads, unsigned tid) {
   if (len == 0) return;
   const unsigned mis = (unsigned)((uintptr_t)dst & 15);
   uint8_t* dbase = dst - mis;
@@ -410,14 +414,14 @@ __device__ __forceinline__ void copy_out(uint8_t* __restrict__ dst, const uint8_
   // (bs == 0 for every other tile of 2-byte output: those copy whole words
   // without the four funnel shifts per chunk)
   switch ((rel >> 2) | (bs ? 4u : 0u)) {
-    case 0: copy_out_ws<0, false>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 1: copy_out_ws<1, false>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 2: copy_out_ws<2, false>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 3: copy_out_ws<3, false>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 4: copy_out_ws<0, true>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 5: copy_out_ws<1, true>(dbase, sbase, mis, len, bs, nthreads); break;
-    case 6: copy_out_ws<2, true>(dbase, sbase, mis, len, bs, nthreads); break;
-    default: copy_out_ws<3, true>(dbase, sbase, mis, len, bs, nthreads); break;
+    case 0: copy_out_ws<0, false>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 1: copy_out_ws<1, false>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 2: copy_out_ws<2, false>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 3: copy_out_ws<3, false>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 4: copy_out_ws<0, true>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 5: copy_out_ws<1, true>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    case 6: copy_out_ws<2, true>(dbase, sbase, mis, len, bs, nthreads, tid); break;
+    default: copy_out_ws<3, true>(dbase, sbase, mis, len, bs, nthreads, tid); break;
   }
 }
 

@@ -36,6 +36,12 @@ namespace vt {
 #define VT_GRAB_AT_U16 10  // cfg3 A/B (r1n): 8 1.100, 9 1.087, 10 1.077, 11 1.082, 12 1.081 ms
 #endif
 
+// VT_LB_COPY: the look-back warp copies the staged tile out (it holds none of
+// the tile's words, so its copy loop has the registers to itself, and the
+// compute warps go from count straight to decode)
+#ifndef VT_LB_COPY
+#define VT_LB_COPY 1
+#endif
 #ifndef VT_SCAN1
 #define VT_SCAN1 0  // one-barrier block scan (block_excl_scan1)
 #endif
@@ -139,12 +145,14 @@ static_assert(offsetof(PipeSmem<PipeTailProbe>, excl) + 16 - offsetof(PipeSmem<P
 
 template <class C>
 __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const uint8_t* stage,
-                                              unsigned long long excl, unsigned agg) {
+                                              unsigned long long excl, unsigned agg,
+                                              unsigned nthreads = kComputeThreads,
+                                              unsigned tid = threadIdx.x) {
   if (excl == ~0ull) return;  // a tile before this one failed: output is dead
 #if VT_CHECKS
   if ((excl + agg) * C::kOutBytes > a.out_cap)
     vt_check_fail("copy-out", excl * C::kOutBytes, (unsigned long long)agg * C::kOutBytes, 0, a.out_cap);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     // the staged bytes the copy-out reads lie inside the staging region
     uint32_t dsz;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
@@ -157,7 +165,7 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
   return;
 #endif
   copy_out(reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes, stage, agg * C::kOutBytes,
-           kComputeThreads);
+           nthreads, tid);
 }
 
 // Hand-off barriers (all kPipeBlock threads), indexed by the CTA-local tile
@@ -211,9 +219,23 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
   if (threadIdx.x == 0) VT_TR_MIN(0);
   if (threadIdx.x >= kComputeThreads) {
     const bool leader = threadIdx.x == kComputeThreads;
+#if VT_LB_COPY
+    unsigned long long excl_prev = 0;
+    unsigned agg_prev = 0;
+#endif
     for (unsigned j = 0;; j++) {
       bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
       const unsigned tile = sm.lb_tile[j & 3];
+#if VT_LB_COPY
+      // tile j-1 is staged completely (the compute warps arrive on GRAB(j)
+      // after its decode) and its offset was resolved in the previous round:
+      // copy it out, then hand the buffer back (EXCL(j-1) = "copy done")
+      if (j > 0) {
+        copy_tile_out<C>(a, sm.out[(j - 1) % NS], excl_prev, agg_prev, 32u, threadIdx.x - kComputeThreads);
+        // (after the CTA's last tile nobody waits for the buffer)
+        if (tile < a.ntiles) bar_arrive(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
+      }
+#endif
       if (tile >= a.ntiles) break;
       unsigned long long excl = 0;
       if (tile != 0) {
@@ -239,7 +261,12 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       }
 #endif
       if (leader) sm.excl[j & 1] = excl;
+#if VT_LB_COPY
+      excl_prev = excl;
+      agg_prev = sm.agg[j & 1];
+#else
       bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
+#endif
     }
   } else {
     // compute warps
@@ -266,7 +293,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         atomicAdd(&a.ctl->pad[3], 1ull);
       }
 #endif
+#if !VT_LB_COPY
       copy_tile_out<C>(a, sm.out[(j - 1) % NS], sm.excl[(j - 1) & 1], prev_agg);
+#endif
       VT_PH(3);
     };
     while (true) {
@@ -327,7 +356,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
           sm.tile = t;
           sm.lb_tile[(j + 1) & 3] = t;
         }
+#if !VT_LB_COPY
         ComputeSync::sync();  // the buffer is free (and the next tile id is out)
+#endif
         VT_PH(4);
         if (VT_DEAD_SKIP && sm.dead) agg = 0;  // (nothing staged, nothing to copy out)
         // the look-back gave up on tile j-1: it lies behind an error, and so
@@ -380,7 +411,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       prev_agg = agg;
       j++;
     }
+#if !VT_LB_COPY
     if (j > 0) copy_prev();
+#endif
     if (threadIdx.x == 0) VT_TR_MAX(5);
   }
   finalize_if_last(a, true, C::kTileElems);
