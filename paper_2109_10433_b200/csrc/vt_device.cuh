@@ -72,7 +72,10 @@ __device__ __forceinline__ unsigned long long vt_gtimer() {
 extern __shared__ __align__(16) uint8_t vt_dyn_smem[];
 // bytes of PipeSmem after its staging region (scan .. excl, vt_pipeline.cuh
 // static_asserts it): a staging store must land before them
-constexpr unsigned kPipeTail = 120;
+#ifndef VT_COMPUTE_THREADS
+#define VT_COMPUTE_THREADS 256
+#endif
+constexpr unsigned kPipeTail = 8 * (VT_COMPUTE_THREADS / 32) + 56;
 
 static __device__ __noinline__ void vt_check_fail(const char* what, unsigned long long a,
                                                   unsigned long long b, unsigned long long lo,
