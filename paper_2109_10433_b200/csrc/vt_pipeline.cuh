@@ -14,11 +14,16 @@
 //   emit(a, tc, stage, off)  write this thread's output at stage + off
 //
 // transcode_body is the kernel body: warp-specialised.  Warps 0..7 count tile
-// j and decode it into the staging buffer, then copy it to global memory during
-// tile j+1, once warp 8 has resolved its offset with the decoupled look-back
-// (started when tile j was taken).  Tiles are taken in order, one at a time per
-// CTA.  (Validation and lengths need no offsets and use the barrier-free row
-// kernels in k_utf8.cu / k_utf16.cu.)
+// j and decode it into the staging buffer.  Warp 8 resolves tile j's offset with
+// the decoupled look-back (started when tile j was taken) and, once the compute
+// warps have decoded it (they arrive on the next tile's GRAB barrier), copies
+// the staged tile to global memory itself while the compute warps count tile
+// j+1 -- it holds none of the tile's words, so its copy loop has the registers
+// the compute warps do not have (VT_LB_COPY; with 0 the compute warps copy tile
+// j-1 out between the count and the decode of tile j, the round-1 form).
+// Tiles are taken in order, one at a time per CTA.  (Validation and lengths
+// need no offsets and use the barrier-free row kernels in k_utf8.cu /
+// k_utf16.cu.)
 #pragma once
 
 #include <cstddef>
@@ -176,9 +181,10 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
 //   BAR_AGG + (j & 1):  compute warps arrive once tile j's aggregate is in
 //             shared memory; the look-back warp waits, publishes tile j's
 //             inclusive prefix;
-//   BAR_EXCL + (j & 1): the look-back warp arrives once tile j's offset is in
-//             shared memory; the compute warps wait before copying tile j out
-//             (during tile j+1).
+//   BAR_EXCL + (j & 1): the look-back warp arrives once it has copied tile j
+//             out (VT_LB_COPY; otherwise once tile j's offset is in shared
+//             memory); the compute warps wait before they decode tile j+1
+//             into the same buffer (otherwise: before copying tile j out).
 // bar.arrive orders the producer's prior shared-memory writes before the
 // consumer's bar.sync returns, and a waiting warp issues nothing (no polling).
 // At most one instance per id is pending:
