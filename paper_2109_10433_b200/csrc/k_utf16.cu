@@ -208,6 +208,7 @@ struct TileCount16 {
   long long v0;
   unsigned lo, lim;
   bool simple;
+  bool ascii;  // interior tile and the thread's 32 units are ASCII (emit_ascii_row16)
   unsigned cnt;
 };
 
@@ -274,6 +275,8 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
   }
   tc.lim = hi;
   const Class16 c = classify16(tc.W);
+  // (every unit >= 0x80 adds at least one byte: 32 bytes <=> 32 ASCII units)
+  tc.ascii = kTranscode && interior && c.bytes == K16_UPT;
   unsigned my_err = kNone16;
   if (c.err) {
     const Words16 tmp = tc.W;  // (a copy: tc.W itself stays in registers)
@@ -364,8 +367,39 @@ struct Utf16Codec {
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
-                                              unsigned off, Mid&& mid) {
-    if (tc.simple) {
+                                              unsigned off, unsigned tile, Mid&& mid) {
+    if (tc.simple && __all_sync(0xffffffffu, tc.ascii)) {
+      // A warp whose 1024 units are all ASCII: every lane writes exactly 32
+      // bytes, the lanes' addresses are 32 bytes apart and the byte stores of
+      // the general path conflict 8-way (and more so the stores of one lane
+      // land in few words).  Each lane packs four units into one word and
+      // stores its eight words in a lane-dependent order (re-read from global
+      // memory, an L1 hit), so that the 32 words of one store fall into 32
+      // different banks.  Warp-uniform alignment: the lanes are 32 bytes apart.
+      const unsigned lane = threadIdx.x & 31;
+      const uint2* p = reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(a.base) +
+                                                      (size_t)tile * (2 * K16_TILE) +
+                                                      (size_t)(2 * K16_UPT * threadIdx.x));
+      const uint32_t qb = smem_addr(stage) + off;
+      const bool aligned4 = (qb & 3u) == 0;
+#pragma unroll 4
+      for (unsigned k = 0; k < (unsigned)K16_WPT / 2; k++) {
+        const unsigned j = (k + (lane >> 2)) & (K16_WPT / 2 - 1);
+        const uint2 x = __ldg(p + j);
+        const uint32_t w = prmt(x.x, x.y, kBE ? 0x7531 : 0x6420);  // the four low bytes
+        const uint32_t q = qb + 4u * j;
+        if (aligned4) {
+          VT_CHECK_STS(q, 4);
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(q), "r"(w));
+        } else {
+          sts8(q, w);
+          sts8(q + 1, w >> 8);
+          sts8(q + 2, w >> 16);
+          sts8(q + 3, w >> 24);
+        }
+      }
+      mid();
+    } else if (tc.simple) {
       // (tc.lo > 0 only for the first thread of a call: the zeros before the
       // input are encoded too and land in the pad before the staging buffer)
       uint32_t q = smem_addr(stage) + off - tc.lo;

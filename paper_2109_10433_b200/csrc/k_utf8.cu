@@ -560,6 +560,7 @@ struct TileCount {
   unsigned lo, lim;  // in-input positions [lo, lim) of the thread (clipped at the tile's error)
   bool simple;       // interior tile without error: SWAR emission from W
   bool four;         // the thread has 4-byte characters
+  bool ascii;        // interior tile and the thread's 64 bytes are ASCII (emit_ascii_row)
   unsigned cnt;      // units (transcode) or characters of the thread
 };
 
@@ -609,6 +610,12 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
 #endif
   tc.four = co.four;
   tc.lim = hi;
+  // all 64 bytes ASCII: no continuation byte and no 4-byte lead in the thread
+  // (then any other lead would need its continuation inside the thread, or
+  // the structure check fails) and the last byte is not a lead whose
+  // continuation belongs to the next thread
+  tc.ascii = !kNV && interior && co.chars == K8_BPT && co.units == K8_BPT &&
+             (tc.W.w[K8_WPT] & 0x80000000u) == 0;
   unsigned my_err = kNone;
   if (co.viol) {
     const Words tmp = tc.W;  // (a copy: tc.W itself stays in registers)
@@ -651,9 +658,48 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
 }
 
 // ---- per-tile back half: decode into the staging buffer -----------------------
+// A warp whose 2 KiB row is all ASCII.  Every lane then writes exactly 128
+// bytes, so the lanes' staging addresses are 128 bytes apart: all 32 in one
+// bank, and the per-word stores of the general path conflict 32-way (measured:
+// pure ASCII ran at 4.0 ms per GiB against 0.8 for mixed text).  Here lane t
+// handles its words in the order t, t+1, ... (mod 16) -- re-read from global
+// memory (an L1 hit), since registers cannot be indexed by lane -- which
+// spreads the lanes of one store over 16 bank pairs.  Warp-uniform: the row's
+// alignment in the staging buffer is the same for every lane.
+template <bool kBE>
+__device__ __forceinline__ void emit_ascii_row(const U8Args& a, unsigned tile, uint16_t* stage,
+                                               unsigned off) {
+  const unsigned lane = threadIdx.x & 31;
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(a.base + (size_t)tile * K8_TILE +
+                                                        (size_t)(K8_BPT * threadIdx.x));
+  const uint32_t qb = smem_addr(stage) + 2u * off;
+  const bool aligned4 = (qb & 2u) == 0;  // (same for every lane: off = row start + 64 * lane)
+#pragma unroll 4
+  for (unsigned k = 0; k < (unsigned)K8_WPT; k++) {
+    const unsigned j = (k + lane) & (K8_WPT - 1);
+    const uint32_t x = __ldg(p + j);
+    const uint32_t u01 = prmt(x, 0, kBE ? 0x1404 : 0x4140), u23 = prmt(x, 0, kBE ? 0x3424 : 0x4342);
+    const uint32_t q = qb + 8u * j;
+    if (aligned4) {
+      VT_CHECK_STS(q, 8);
+      asm volatile("st.shared.u32 [%0], %1;\n\tst.shared.u32 [%0+4], %2;" ::"r"(q), "r"(u01), "r"(u23));
+    } else {
+      sts16(q, u01);
+      sts16(q + 2, u01 >> 16);
+      sts16(q + 4, u23);
+      sts16(q + 6, u23 >> 16);
+    }
+  }
+}
+
 template <bool kBE, bool kNV, class Mid>
 __device__ __forceinline__ void emit_tile(const U8Args& a, const TileCount& tc, uint16_t* stage,
-                                          unsigned off, Mid&& mid) {
+                                          unsigned off, unsigned tile, Mid&& mid) {
+  if (tc.simple && __all_sync(0xffffffffu, tc.ascii)) {
+    emit_ascii_row<kBE>(a, tile, stage, off);
+    mid();
+    return;
+  }
   if (tc.simple) {
     // (tc.lo > 0 only for the first thread of a call: the zeros before the
     // input are decoded too and land in the pad before the staging buffer)
@@ -722,8 +768,8 @@ struct Utf8Codec {
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
-                                              unsigned off, Mid&& mid) {
-    emit_tile<kBE, kNV>(a, tc, reinterpret_cast<uint16_t*>(stage), off, mid);
+                                              unsigned off, unsigned tile, Mid&& mid) {
+    emit_tile<kBE, kNV>(a, tc, reinterpret_cast<uint16_t*>(stage), off, tile, mid);
   }
 };
 

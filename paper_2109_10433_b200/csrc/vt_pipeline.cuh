@@ -11,7 +11,7 @@
 //       load + validate + count the tile; off = this thread's exclusive
 //       output offset, agg = the tile's output (elements); errors reported
 //       through atomicMin(&ctl->err) and clipped out of the counts
-//   emit(a, tc, stage, off)  write this thread's output at stage + off
+//   emit(a, tc, stage, off, tile, mid)  write this thread's output at stage + off
 //
 // transcode_body is the kernel body: warp-specialised.  Warps 0..7 count tile
 // j and decode it into the staging buffer.  Warp 8 resolves tile j's offset with
@@ -389,7 +389,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       if (dead || (VT_DEAD_SKIP && NS == 1 && j > 0 && sm.dead))
         grab();
       else
-        C::emit(a, tc, sm.out[j % NS], off, grab);
+        C::emit(a, tc, sm.out[j % NS], off, sm.lb_tile[j & 3], grab);
 #else
       grab();
 #endif

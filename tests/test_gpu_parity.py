@@ -552,3 +552,72 @@ def test_utf16be_paths(oracle, torch):
     want, wr = oracle.utf8_to_utf16(d_in[:n].cpu().numpy())
     assert _same(r, wr)
     assert np.array_equal(d16[: r.written].cpu().numpy().view(np.uint16), want.byteswap())
+
+
+def test_ascii_rows(oracle, torch):
+    """Warps whose whole 2 KiB row (1024 units) is ASCII take their own staging
+    path (lane-rotated word order, k_utf8.cu emit_ascii_row / k_utf16.cu): pure
+    ASCII over many tiles at every input alignment and several output
+    alignments, ASCII with one non-ASCII character or one error per few rows
+    (mixed warps next to ASCII warps), a 2- / 4-byte lead in a thread's last
+    byte, both directions, little and big endian."""
+    rng = np.random.default_rng(23)
+    n = 5 * 16384 + 777
+    base = rng.integers(0x20, 0x7F, n, dtype=np.uint8)
+    variants = [("pure", base)]
+    v = base.copy()
+    for p in range(3000, n - 2600, 5000):  # sparse 2- and 3-byte characters
+        v[p:p + 2] = (0xC3, 0xA9)
+        v[p + 2500:p + 2503] = (0xE4, 0xB8, 0xAD)
+    variants.append(("sparse", v))
+    v = base.copy()
+    for t in range(1, 5):  # leads in the last byte of a thread's 64 (at offset 0 alignment)
+        p = 16384 * t + 64 * 7 + 63
+        v[p:p + 2] = (0xC3, 0xA9)
+        p = 16384 * t + 64 * 40 + 63
+        v[p:p + 4] = (0xF0, 0x9F, 0x98, 0x80)
+    variants.append(("edge-leads", v))
+    v = base.copy()
+    v[40000] = 0x80  # stray continuation in an otherwise ASCII tile
+    variants.append(("error", v))
+    buf = torch.zeros(n + 64, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(2 * n + 128, dtype=torch.uint8, device="cuda")
+    for name, data in variants:
+        want16, want = oracle.utf8_to_utf16(data)
+        for off in (0, 1, 2, 3, 5, 8, 13, 15):
+            arr = np.zeros(n + 64, dtype=np.uint8)
+            arr[off:off + n] = data
+            buf.copy_(torch.from_numpy(arr))
+            for ooff in (0, 2, 6):
+                out.fill_(0xEE)
+                r = vt.utf8_to_utf16_device(buf, n, out[ooff:].view(torch.int16), offset=off)
+                assert _same(r, want), (name, off, ooff)
+                got = out[ooff:ooff + 2 * r.written].cpu().numpy().view("<u2")
+                assert np.array_equal(got, want16[: r.written]), (name, off, ooff)
+        # big-endian output through the host entry point
+        o_be, r_be = vt.utf8_to_utf16be(bytes(data))
+        assert _same(r_be, want) and np.array_equal(o_be, want16.byteswap()[: r_be.written]), name
+        if want.error_at is not None:
+            continue
+        # back: UTF-16 -> UTF-8 (the ASCII rows of that kernel), LE at several alignments, BE via host
+        u = want16
+        ubuf = torch.zeros(len(u) + 32, dtype=torch.int16, device="cuda")
+        o8 = torch.zeros(3 * len(u) + 64, dtype=torch.uint8, device="cuda")
+        want8, w8 = oracle.utf16_to_utf8(u)
+        for uoff in (0, 1, 3, 7):
+            arr = np.zeros(len(u) + 32, dtype=np.uint16)
+            arr[uoff:uoff + len(u)] = u
+            ubuf.copy_(torch.from_numpy(arr.view(np.int16)))
+            for ooff in (0, 1, 2, 3):
+                o8.fill_(0xEE)
+                r = vt.utf16_to_utf8_device(ubuf, len(u), o8[ooff:], offset=2 * uoff)
+                assert _same(r, w8), (name, uoff, ooff)
+                assert np.array_equal(o8[ooff:ooff + r.written].cpu().numpy(), want8), (name, uoff, ooff)
+        ob, rb = vt.utf16be_to_utf8(u.byteswap())
+        assert _same(rb, w8) and np.array_equal(ob, want8), name
+    # a lone surrogate in an ASCII UTF-16 stream
+    u = base[: 3 * 8192 + 100].astype(np.uint16)
+    u[9000] = 0xDC00
+    want8, w8 = oracle.utf16_to_utf8(u)
+    o, r = vt.utf16_to_utf8(u)
+    assert _same(r, w8) and np.array_equal(o, want8)
