@@ -26,7 +26,7 @@ LIB = os.path.join(LIBDIR, "libvtrans_gpu.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["k_utf8.cu", "k_utf16.cu", "k_batch.cu", "k_datagen.cu", "k_stream.cu", "runtime.cu"]
 CXX_SOURCES = ["shim.cpp"]
-HEADERS = ["vt_device.cuh", "vt_kernels.h", "vt_gen.cuh", "vt_pipeline.cuh"]
+HEADERS = ["vt_device.cuh", "vt_kernels.h", "vt_gen.cuh", "vt_pipeline.cuh", "vt_swar.cuh"]
 
 
 def nvcc() -> str:
