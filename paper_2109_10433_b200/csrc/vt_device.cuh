@@ -229,101 +229,56 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
                                                       unsigned tile, const Ctl* ctl,
                                                       unsigned long long tile_bytes,
                                                       unsigned long long head) {
-  constexpr int K = VT_LB_WIN;
+  // (One window of 32 status words per step.  The look-back warp also copies
+  // the tiles out, and it gets one warp's share of its scheduler's issue slots,
+  // so every instruction here delays the hand-back of the staging buffer:
+  // 32-bit tags and sums, REDUX instead of shuffle trees, no per-window arrays.)
   const unsigned lane = threadIdx.x & 31;
   const unsigned ep = epoch & 0x3FFF;
+  const unsigned tag_agg = 0x4000u | ep, tag_pre = 0x8000u | ep;
   unsigned long long excl = 0;
-  long long base = (long long)tile - 1;  // newest predecessor not yet summed
+  int base = (int)tile - 1;  // newest predecessor not yet summed (tiles < 2^31)
 #if VT_LB_DELAY
   // the predecessor was taken just before this tile and publishes its
   // aggregate only after its count phase (~4 us): polling before that only
-  // loads the status lines (measured 0.915 -> 0.910 ms cfg2 with 2.5-4 us)
-  // (not in the first two waves of tiles: small inputs are latency-bound)
+  // loads the status lines (not in the first two waves of tiles: small inputs
+  // are latency-bound)
   if (tile >= 2 * gridDim.x) __nanosleep(VT_LB_DELAY);
 #endif
   for (bool first = true;; first = false) {
     // a tile behind a known error is dead: give up (its output is never read;
     // the tail of an early-error call waits on these look-backs).  Checked at
     // the start, beside the first status loads (same round trip), and
-    // whenever a poll makes no progress (below); checking on every poll costs
-    // the hot path ~0.7 % (everyone hits the error word's line).
+    // whenever a poll makes no progress (below).
     const unsigned long long err =
         first && lane == 0 ? load_relaxed(const_cast<unsigned long long*>(&ctl->err)) : kNoError;
-    unsigned long long v[K];
-    bool rdy[K], pre[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-      const long long idx = base - 32 * k - (long long)lane;
-      const unsigned long long st = idx >= 0 ? load_status(&status[idx]) : 0ull;
-      rdy[k] = idx < 0 || (((st >> 62) != 0) && (((st >> 48) & 0x3FFF) == ep));
-      pre[k] = idx < 0 || (rdy[k] && (st >> 62) == 2);  // before tile 0: prefix 0
-      v[k] = idx < 0 ? 0ull : (st & kValMask);
-    }
-    {
+    const int idx = base - (int)lane;
+    const unsigned long long st = idx >= 0 ? load_status(&status[idx]) : 0ull;
+    const unsigned tag = (unsigned)(st >> 48);
+    const bool pre = idx < 0 || tag == tag_pre;  // before tile 0: prefix 0
+    const bool rdy = pre || tag == tag_agg;
+    const uint32_t v32 = idx < 0 ? 0u : (uint32_t)st;  // aggregates are tile-sized: 32 bits
+    if (first) {
       const unsigned long long e = __shfl_sync(0xffffffffu, err, 0);
       if (e != kNoError && (e + head) / tile_bytes < tile) return ~0ull;
     }
-    uint32_t wsum[K];  // window sums of the fully-ready windows passed so far
-    int k = 0;
-    unsigned run = 0;
-#pragma unroll
-    for (int kk = 0; kk < K; kk++) {
-      k = kk;
-      const unsigned rm = __ballot_sync(0xffffffffu, rdy[kk]);
-      const unsigned pm = __ballot_sync(0xffffffffu, pre[kk]);
-      run = rm == 0xffffffffu ? 32u : (unsigned)__ffs(~rm) - 1u;
-      const unsigned pre_in = pm & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
-      if (pre_in) {
-        const unsigned stop = (unsigned)__ffs(pre_in) - 1u;  // nearest inclusive prefix
-        const unsigned long long pval = __shfl_sync(0xffffffffu, v[kk], stop);
-        // window k: suffix sums over lanes [lane, stop)
-        uint32_t x = lane < stop ? (uint32_t)v[kk] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
-          if (lane + o < 32) x += y;
-        }
-        if (lane < stop)
-          if (VT_LB_HELP)
-            store_status(&status[base - 32 * kk - lane], pack_status(kFlagPre, epoch, pval + x));
-        unsigned long long newer = pval + __shfl_sync(0xffffffffu, x, 0);  // prefix through window k
-        // windows k-1 .. 0 (fully ready, summed): their tiles' inclusive prefixes
-#pragma unroll
-        for (int j = kk - 1; j >= 0; j--) {
-          uint32_t z = (uint32_t)v[j];
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_down_sync(0xffffffffu, z, o);
-            if (lane + o < 32) z += y;
-          }
-          if (VT_LB_HELP)
-            store_status(&status[base - 32 * j - lane], pack_status(kFlagPre, epoch, newer + z));
-          newer += wsum[j];
-        }
-        return excl + newer;
-      }
-      if (run < 32) break;
-      wsum[kk] = __reduce_add_sync(0xffffffffu, (uint32_t)v[kk]);
-      k = kk + 1;
+    const unsigned rm = __ballot_sync(0xffffffffu, rdy);
+    const unsigned pm = __ballot_sync(0xffffffffu, pre);
+    const unsigned run = rm == 0xffffffffu ? 32u : (unsigned)__ffs(~rm) - 1u;
+    const unsigned pre_in = pm & (run == 32 ? 0xffffffffu : ((1u << run) - 1u));
+    if (pre_in) {
+      const unsigned stop = (unsigned)__ffs(pre_in) - 1u;  // nearest inclusive prefix
+      const unsigned long long pval =
+          __shfl_sync(0xffffffffu, idx < 0 ? 0ull : (st & kValMask), stop);
+      const uint32_t s = __reduce_add_sync(0xffffffffu, lane < stop ? v32 : 0u);
+      return excl + pval + s;
     }
 #ifdef VT_PROBE
-    if (lane == 0) atomicAdd(const_cast<unsigned long long*>(&ctl->pad[4]), (k > 0 || run > 0) ? (1ull << 32) : 1ull);
+    if (lane == 0) atomicAdd(const_cast<unsigned long long*>(&ctl->pad[4]), run > 0 ? (1ull << 32) : 1ull);
 #endif
-    // no prefix in reach: bank the ready part (windows 0..k-1, then `run` lanes of k)
-#pragma unroll
-    for (int j = 0; j < K; j++)
-      if (j < k) excl += wsum[j];
-    unsigned long long adv = 32ull * k;
-    if (k < K && run > 0) {
-      uint32_t part = 0;
-#pragma unroll
-      for (int j = 0; j < K; j++)
-        if (j == k) part = __reduce_add_sync(0xffffffffu, lane < run ? (uint32_t)v[j] : 0u);
-      excl += part;
-      adv += run;
-    }
-    if (adv > 0) {
-      base -= (long long)adv;
+    if (run > 0) {  // no prefix in reach: bank the ready part and walk on
+      excl += __reduce_add_sync(0xffffffffu, lane < run ? v32 : 0u);
+      base -= (int)run;
       continue;
     }
     // nothing ready yet: give up if an earlier tile failed (our output is dead)
