@@ -181,6 +181,9 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
 //   BAR_AGG + (j & 1):  compute warps arrive once tile j's aggregate is in
 //             shared memory; the look-back warp waits, publishes tile j's
 //             inclusive prefix;
+//   BAR_DONE + (j & 1): compute warps arrive once tile j is decoded into the
+//             staging buffer (VT_LB_COPY); the look-back warp waits, then
+//             copies it out;
 //   BAR_EXCL + (j & 1): the look-back warp arrives once it has copied tile j
 //             out (VT_LB_COPY; otherwise once tile j's offset is in shared
 //             memory); the compute warps wait before they decode tile j+1
@@ -197,7 +200,7 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
 //     only after its wait on GRAB(j+2) or GRAB(j+1), so after GRAB(j) -- two
 //     ids per kind are not enough for GRAB with two buffers, where GRAB(j+2)
 //     is arrived at while the look-back warp may still be before GRAB(j+1).
-constexpr int BAR_EXCL = 2, BAR_AGG = 4, BAR_GRAB = 8;
+constexpr int BAR_EXCL = 2, BAR_AGG = 4, BAR_GRAB = 8, BAR_DONE = 6;
 
 #ifdef VT_PHASES
 // per-phase cycle totals of warp 0 of every CTA (perf probe): loop-top sync,
@@ -230,19 +233,24 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
     unsigned agg_prev = 0;
 #endif
     for (unsigned j = 0;; j++) {
-      bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
-      const unsigned tile = sm.lb_tile[j & 3];
 #if VT_LB_COPY
-      // tile j-1 is staged completely (the compute warps arrive on GRAB(j)
-      // after its decode) and its offset was resolved in the previous round:
-      // copy it out, then hand the buffer back (EXCL(j-1) = "copy done")
+      // tile j-1 is staged completely (the compute warps arrive on DONE(j-1)
+      // right after its decode, before the next tile's id is known) and its
+      // offset was resolved in the previous round: copy it out, then hand the
+      // buffer back (EXCL(j-1) = "copy done")
       if (j > 0) {
+        bar_sync(BAR_DONE + ((j - 1) & 1), kPipeBlock);
         copy_tile_out<C>(a, sm.out[(j - 1) % NS], excl_prev, agg_prev, 32u, threadIdx.x - kComputeThreads);
-        // (after the CTA's last tile nobody waits for the buffer)
-        if (tile < a.ntiles) bar_arrive(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
       }
 #endif
+      bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
+      const unsigned tile = sm.lb_tile[j & 3];
       if (tile >= a.ntiles) break;
+#if VT_LB_COPY
+      // (the compute warps wait for the buffer only after counting tile j; after
+      // the CTA's last tile nobody waits, so the arrival comes behind the break)
+      if (j > 0) bar_arrive(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
+#endif
       unsigned long long excl = 0;
       if (tile != 0) {
 #ifdef VT_PROBE
@@ -392,6 +400,11 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         C::emit(a, tc, sm.out[j % NS], off, sm.lb_tile[j & 3], grab);
 #else
       grab();
+#endif
+#if VT_LB_COPY
+      // tile j is staged: the look-back warp may copy it out now, while thread 0
+      // still waits for the next tile's id (the atomic's round trip)
+      bar_arrive(BAR_DONE + (j & 1), kPipeBlock);
 #endif
       VT_PH(5);
 #ifdef VT_TRACE
