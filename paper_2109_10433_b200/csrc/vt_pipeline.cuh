@@ -47,6 +47,18 @@ namespace vt {
 #ifndef VT_LB_COPY
 #define VT_LB_COPY 1
 #endif
+// VT_BULK_COPY (with VT_LB_COPY, one staging buffer): the staged tile leaves as
+// ONE asynchronous bulk copy (cp.async.bulk shared -> global, the TMA unit)
+// issued by the look-back warp's leader, not as a copy loop.  A bulk copy needs
+// source, destination and size in whole 16-byte chunks, and a tile's output
+// starts at any element: so the compute warps wait for the tile's own offset
+// before the decode (the look-back of tile j runs while tile j is counted, and
+// overlaps the bulk copy of tile j-1) and stage the tile at the phase of its
+// global address, (out + excl) & 15.  The look-back warp's lanes store the
+// partial chunks at both ends themselves (< 16 bytes each).
+#ifndef VT_BULK_COPY
+#define VT_BULK_COPY 0
+#endif
 #ifndef VT_SCAN1
 #define VT_SCAN1 0  // one-barrier block scan (block_excl_scan1)
 #endif
@@ -127,7 +139,7 @@ __device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems
 template <class C>
 struct PipeSmem {
   alignas(16) uint8_t pad0[32];
-  alignas(16) uint8_t out[C::kNStage][C::kStageBytes + 32];
+  alignas(16) uint8_t out[C::kNStage][C::kStageBytes + 48];  // (+16: the staging phase)
   alignas(16) uint8_t pad1[32];
   unsigned scan[kComputeThreads / 32];
   unsigned red[kComputeThreads / 32];
@@ -171,6 +183,60 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
 #endif
   copy_out(reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes, stage, agg * C::kOutBytes,
            nthreads, tid);
+}
+
+// Writers of shared memory that an asynchronous (bulk) copy will read: orders
+// their generic-proxy stores before the async proxy's reads (with the barrier
+// that follows).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// (leader) the bulk copies issued so far have read their shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// The staged tile (at stage + phase, phase = the low four bits of its global
+// address) to global memory, by one warp: whole 16-byte chunks as one bulk copy
+// (lane 0), the partial chunk before them by lanes 0..15 and the one behind
+// them by lanes 16..31, a byte each.
+template <class C>
+__device__ __forceinline__ void bulk_tile_out(const typename C::Args& a, const uint8_t* stage0,
+                                              unsigned long long excl, unsigned agg, unsigned lane) {
+  if (excl == ~0ull || agg == 0) return;  // a tile before this one failed: output is dead
+#if VT_CHECKS
+  if ((excl + agg) * C::kOutBytes > a.out_cap)
+    vt_check_fail("copy-out", excl * C::kOutBytes, (unsigned long long)agg * C::kOutBytes, 0, a.out_cap);
+#endif
+#ifdef VT_EXP_NOCOPY
+  return;
+#endif
+  uint8_t* const d0 = reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes;
+  const unsigned len = agg * C::kOutBytes;
+  const unsigned phase = (unsigned)((uintptr_t)d0 & 15u);
+  // byte positions relative to the 16-byte chunk d0 lies in (= staging offsets)
+  const unsigned end = phase + len;
+  const unsigned body0 = phase ? 16u : 0u;  // first whole chunk
+  const unsigned body1 = end & ~15u;        // behind the last whole chunk
+  uint8_t* const dbase = d0 - phase;
+  const uint32_t sbase = smem_addr(stage0);
+  if (lane == 0 && body1 > body0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                 "cp.async.bulk.commit_group;" ::"l"(__cvta_generic_to_global(dbase + body0)),
+                 "r"(sbase + body0), "r"(body1 - body0)
+                 : "memory");
+  }
+  const unsigned tail0 = body1 > body0 ? body1 : body0;
+  const unsigned pos = lane < 16 ? lane : tail0 + (lane - 16);
+  const bool mine = lane < 16 ? (pos >= phase && pos < (end < body0 ? end : body0)) : pos < end;
+  if (mine) {
+    uint32_t b;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(sbase + pos));
+    dbase[pos] = (uint8_t)b;
+  }
 }
 
 // Hand-off barriers (all kPipeBlock threads), indexed by the CTA-local tile
@@ -240,13 +306,17 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // buffer back (EXCL(j-1) = "copy done")
       if (j > 0) {
         bar_sync(BAR_DONE + ((j - 1) & 1), kPipeBlock);
+#if VT_BULK_COPY
+        bulk_tile_out<C>(a, sm.out[0], excl_prev, agg_prev, threadIdx.x - kComputeThreads);
+#else
         copy_tile_out<C>(a, sm.out[(j - 1) % NS], excl_prev, agg_prev, 32u, threadIdx.x - kComputeThreads);
+#endif
       }
 #endif
       bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
       const unsigned tile = sm.lb_tile[j & 3];
       if (tile >= a.ntiles) break;
-#if VT_LB_COPY
+#if VT_LB_COPY && !VT_BULK_COPY
       // (the compute warps wait for the buffer only after counting tile j; after
       // the CTA's last tile nobody waits, so the arrival comes behind the break)
       if (j > 0) bar_arrive(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
@@ -278,10 +348,20 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #if VT_LB_COPY
       excl_prev = excl;
       agg_prev = sm.agg[j & 1];
+#if VT_BULK_COPY
+      // EXCL(j) = tile j's offset is in shared memory AND the bulk copy of tile
+      // j-1 (in flight during this look-back) has read the staging buffer
+      if (leader) bulk_wait_read();
+      __syncwarp();
+      bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
+#endif
 #else
       bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
 #endif
     }
+#if VT_LB_COPY && VT_BULK_COPY
+    if (leader) bulk_wait_all();  // (the CTA's shared memory must outlive the last copy)
+#endif
   } else {
     // compute warps
     if (threadIdx.x == 0) {
@@ -351,7 +431,27 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       bool dead = false;
       const bool early = VT_GRAB_EARLY && NS == 1 && j > 0;
       if (VT_DEAD_SKIP && threadIdx.x == 0) sm.err_now = err_seen;
-      if (NS == 1 && j > 0) {
+#if VT_LB_COPY && VT_BULK_COPY
+      static_assert(NS == 1 && !VT_GRAB_EARLY && !VT_DEAD_SKIP, "bulk copy-out: one buffer, plain grab");
+      // tile j's own offset (the staging phase) and the buffer, both from the
+      // look-back warp
+      bar_sync(BAR_EXCL + (j & 1), kPipeBlock);
+      VT_PH(2);
+      VT_PH(3);
+      VT_PH(4);
+      const unsigned long long excl_j = sm.excl[j & 1];
+      // the look-back gave up on tile j: it lies behind an error; its decode
+      // and copy-out are skipped
+      if (excl_j == ~0ull) {
+        dead = true;
+        agg = 0;
+      }
+      const unsigned phase =
+          (unsigned)(((uintptr_t)a.out + (uintptr_t)excl_j * (unsigned)C::kOutBytes) & 15u);
+#else
+      const unsigned phase = 0;
+#endif
+      if (!(VT_LB_COPY && VT_BULK_COPY) && NS == 1 && j > 0) {
         if (early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
         // a tile behind an error found meanwhile is dead: its output is never
         // read, so its decode and copy-out are skipped (the load's latency
@@ -397,13 +497,16 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       if (dead || (VT_DEAD_SKIP && NS == 1 && j > 0 && sm.dead))
         grab();
       else
-        C::emit(a, tc, sm.out[j % NS], off, sm.lb_tile[j & 3], grab);
+        C::emit(a, tc, sm.out[j % NS] + phase, off, sm.lb_tile[j & 3], grab);
 #else
       grab();
 #endif
 #if VT_LB_COPY
       // tile j is staged: the look-back warp may copy it out now, while thread 0
       // still waits for the next tile's id (the atomic's round trip)
+#if VT_BULK_COPY
+      fence_proxy_async_smem();
+#endif
       bar_arrive(BAR_DONE + (j & 1), kPipeBlock);
 #endif
       VT_PH(5);
