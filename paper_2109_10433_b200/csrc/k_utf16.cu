@@ -359,10 +359,13 @@ struct Utf16Codec {
   static constexpr int kStageBytes = 3 * K16_TILE;
   static constexpr int kNStage = VT_NSTAGE16;
   static constexpr int kOutBytes = 1;
+  static constexpr int kPrefetchBytes = 0;  // (no input prefetch for this direction)
+  __device__ __forceinline__ static bool prefetchable(const Args&, unsigned) { return false; }
+  __device__ __forceinline__ static const uint8_t* prefetch_src(const Args&, unsigned) { return nullptr; }
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
-                                               unsigned& agg) {
+                                               unsigned& agg, const uint8_t* = nullptr) {
     count_tile16<kTranscode, NT, Sync, kBE>(a, tile, red, scan, tc, off, agg);
   }
   template <class Mid>
@@ -617,6 +620,7 @@ int read_trace16(unsigned long long* out16) {
 int read_phases16(unsigned long long* out8) {
   int rc = (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
   if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 8, g_phase_sub, sizeof(g_phase_sub));
+  if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 12, g_phase_lb, sizeof(g_phase_lb));
   return rc;
 }
 #endif

@@ -567,7 +567,7 @@ struct TileCount {
 template <bool kTranscode, int NT, class Sync, bool kNV = false>
 __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsigned* red,
                                            unsigned* scan, TileCount& tc, unsigned& off,
-                                           unsigned& agg) {
+                                           unsigned& agg, const uint8_t* pf = nullptr) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K8_TILE;  // virtual start of the tile
   // interior: the tile and both halo words lie inside the input.  head < 16, so
@@ -579,7 +579,13 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   const unsigned last_in = endv >= K8_TILE + 4 ? (unsigned)((endv - 4) / K8_TILE) : 0u;  // tiles [1, last_in) are interior
   const bool interior = tile >= 1 && tile < last_in;
   unsigned hi;
-  if (interior) {
+  if (pf) {
+    // prefetched by the pipeline (an interior tile): pf = 16 bytes before the
+    // tile, the tile, 16 bytes behind it, in shared memory
+    load_smem_words<K8_WPT>(smem_addr(pf) + 16u + (unsigned)K8_BPT * threadIdx.x, tc.W.w);
+    tc.lo = 0;
+    hi = K8_BPT;
+  } else if (interior) {
     load_lane_words<K8_WPT>(a.base + (size_t)tile * K8_TILE + (size_t)(K8_BPT * threadIdx.x), lane, tc.W.w);
     tc.lo = 0;
     hi = K8_BPT;
@@ -614,7 +620,7 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
   // (then any other lead would need its continuation inside the thread, or
   // the structure check fails) and the last byte is not a lead whose
   // continuation belongs to the next thread
-  tc.ascii = !kNV && interior && co.chars == K8_BPT && co.units == K8_BPT &&
+  tc.ascii = !kNV && (interior || pf) && co.chars == K8_BPT && co.units == K8_BPT &&
              (tc.W.w[K8_WPT] & 0x80000000u) == 0;
   unsigned my_err = kNone;
   if (co.viol) {
@@ -760,11 +766,20 @@ struct Utf8Codec {
   static constexpr int kStageBytes = 2 * K8_TILE;
   static constexpr int kNStage = VT_NSTAGE8;
   static constexpr int kOutBytes = 2;
+  // input prefetch (vt_pipeline.cuh, VT_PREFETCH): a tile with 16 readable bytes
+  // on either side, copied as [tile start - 16, tile end + 16)
+  static constexpr int kPrefetchBytes = VT_PREFETCH ? K8_TILE + 32 : 0;
+  __device__ __forceinline__ static bool prefetchable(const Args& a, unsigned t) {
+    return t >= 1 && (unsigned long long)(t + 1) * K8_TILE + 16 <= a.head + a.n;
+  }
+  __device__ __forceinline__ static const uint8_t* prefetch_src(const Args& a, unsigned t) {
+    return a.base + (size_t)t * K8_TILE - 16;
+  }
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
-                                               unsigned& agg) {
-    count_tile<kTranscode, NT, Sync, kNV>(a, tile, red, scan, tc, off, agg);
+                                               unsigned& agg, const uint8_t* pf = nullptr) {
+    count_tile<kTranscode, NT, Sync, kNV>(a, tile, red, scan, tc, off, agg, pf);
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,
@@ -986,6 +1001,7 @@ int read_trace8(unsigned long long* out16) {
 int read_phases(unsigned long long* out8) {
   int rc = (int)cudaMemcpyFromSymbol(out8, g_phase, sizeof(g_phase));
   if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 8, g_phase_sub, sizeof(g_phase_sub));
+  if (!rc) rc = (int)cudaMemcpyFromSymbol(out8 + 12, g_phase_lb, sizeof(g_phase_lb));
   return rc;
 }
 #endif

@@ -90,6 +90,12 @@ int device_info(int dev, DeviceInfo& out) {
   d.occ_u8[1] = std::max(1, vt::occupancy_utf8(true));
   d.occ_u16[0] = std::max(1, vt::occupancy_utf16(false));
   d.occ_u16[1] = std::max(1, vt::occupancy_utf16(true));
+  // (perf probe: VT_OCC_CAP=k launches the transcode kernels with at most k CTAs per SM)
+  if (const char* cap = std::getenv("VT_OCC_CAP")) {
+    const int k = std::max(1, std::atoi(cap));
+    d.occ_u8[1] = std::min(d.occ_u8[1], k);
+    d.occ_u16[1] = std::min(d.occ_u16[1], k);
+  }
   if (std::getenv("VT_PRINT_OCC"))
     std::fprintf(stderr, "vtrans: CTAs/SM utf8 validate %d transcode %d, utf16 validate %d transcode %d\n",
                  d.occ_u8[0], d.occ_u8[1], d.occ_u16[0], d.occ_u16[1]);

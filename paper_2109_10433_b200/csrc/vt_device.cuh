@@ -409,6 +409,20 @@ __device__ __forceinline__ void load_lane_words(const uint8_t* p, unsigned lane,
   w[NW + 1] = lane == 31 ? h : nw;
 }
 
+// The same words from a tile prefetched into shared memory (q = the lane's
+// first byte; the words before and behind it are in the buffer too).
+template <int NW>
+__device__ __forceinline__ void load_smem_words(uint32_t q, uint32_t* w) {
+  static_assert(NW % 4 == 0, "whole 16-byte loads");
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(q - 4u));
+#pragma unroll
+  for (int r = 0; r < NW / 4; r++)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[1 + 4 * r]), "=r"(w[2 + 4 * r]), "=r"(w[3 + 4 * r]), "=r"(w[4 + 4 * r])
+                 : "r"(q + 16u * r));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[NW + 1]) : "r"(q + 4u * NW));
+}
+
 // proj/src/codec_core.cpp:5-38 on a 4-byte window (bytes past the input are
 // zero, which fails exactly like the truncation test at :28).
 __device__ __forceinline__ bool decode_ok(uint32_t v) {

@@ -59,6 +59,15 @@ namespace vt {
 #ifndef VT_BULK_COPY
 #define VT_BULK_COPY 0
 #endif
+// VT_PREFETCH (codecs with kPrefetchBytes > 0): the next tile's input arrives in
+// shared memory by one bulk copy (TMA unit) while the current tile is decoded.
+// Thread 0 takes the next tile right after publishing the aggregate (the
+// atomic's round trip overlaps the wait for the staging buffer), starts the
+// copy before the decode, and the next count phase reads its words from shared
+// memory: neither the tile id nor the input loads are waited for.
+#ifndef VT_PREFETCH
+#define VT_PREFETCH 0
+#endif
 #ifndef VT_SCAN1
 #define VT_SCAN1 0  // one-barrier block scan (block_excl_scan1)
 #endif
@@ -138,6 +147,11 @@ __device__ __forceinline__ unsigned grab_tile(const Args& a, unsigned tile_elems
 // CTAs with one buffer beat 3 CTAs with two, 1.12 vs 1.18 ms per GiB).
 template <class C>
 struct PipeSmem {
+  // input prefetch (VT_PREFETCH): transaction barrier, the tile the buffer holds
+  // (or will hold), the buffer: 16 bytes before the tile, the tile, 16 behind
+  alignas(16) unsigned long long mbar;
+  unsigned pf_tile, pf_pad;
+  alignas(16) uint8_t in[C::kPrefetchBytes > 0 ? C::kPrefetchBytes : 16];
   alignas(16) uint8_t pad0[32];
   alignas(16) uint8_t out[C::kNStage][C::kStageBytes + 48];  // (+16: the staging phase)
   alignas(16) uint8_t pad1[32];
@@ -154,7 +168,7 @@ struct PipeSmem {
 
 // (vt_device.cuh's staging-store check assumes this tail size)
 struct PipeTailProbe {
-  static constexpr int kStageBytes = 16, kNStage = 1;
+  static constexpr int kStageBytes = 16, kNStage = 1, kPrefetchBytes = 0;
 };
 static_assert(offsetof(PipeSmem<PipeTailProbe>, excl) + 16 - offsetof(PipeSmem<PipeTailProbe>, scan) ==
                   kPipeTail,
@@ -183,6 +197,32 @@ __device__ __forceinline__ void copy_tile_out(const typename C::Args& a, const u
 #endif
   copy_out(reinterpret_cast<uint8_t*>(a.out) + excl * C::kOutBytes, stage, agg * C::kOutBytes,
            nthreads, tid);
+}
+
+// ---- input prefetch (bulk copy global -> shared with a transaction barrier) ----
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// (one thread) expect `bytes` on the barrier and start the copy that delivers them
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* mbar) {
+  const uint32_t m = smem_addr(mbar);
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];" ::"r"(m),
+      "r"(bytes), "r"(smem_addr(dst)), "l"(__cvta_generic_to_global(src))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
+  const uint32_t m = smem_addr(mbar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "VT_MBAR_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra VT_MBAR_WAIT;\n\t}" ::"r"(m),
+      "r"(parity)
+      : "memory");
 }
 
 // Writers of shared memory that an asynchronous (bulk) copy will read: orders
@@ -275,6 +315,15 @@ __device__ unsigned long long g_phase[8];
 // count sub-phases (thread 0, absolute clocks summed): [0] loads arrived,
 // [1] classify done; read against the count phase's start/end
 __device__ unsigned long long g_phase_sub[4];
+// the look-back warp's leader: wait for the staged tile, copy-out, wait for the
+// next tile id, look-back, wait for the aggregate + publish; [7] = tiles
+__device__ unsigned long long g_phase_lb[8];
+#define VT_PHL(i)                                                              \
+  do {                                                                         \
+    const long long _t = clock64();                                            \
+    if (leader) atomicAdd(&g_phase_lb[i], (unsigned long long)(_t - phl_t));   \
+    phl_t = _t;                                                                \
+  } while (0)
 #define VT_PH(i)                                                  \
   do {                                                            \
     const long long _t = clock64();                               \
@@ -284,6 +333,9 @@ __device__ unsigned long long g_phase_sub[4];
 #else
 #define VT_PH(i) \
   do {           \
+  } while (0)
+#define VT_PHL(i) \
+  do {            \
   } while (0)
 #endif
 
@@ -298,6 +350,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
     unsigned long long excl_prev = 0;
     unsigned agg_prev = 0;
 #endif
+#ifdef VT_PHASES
+    long long phl_t = clock64();
+#endif
     for (unsigned j = 0;; j++) {
 #if VT_LB_COPY
       // tile j-1 is staged completely (the compute warps arrive on DONE(j-1)
@@ -306,6 +361,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // buffer back (EXCL(j-1) = "copy done")
       if (j > 0) {
         bar_sync(BAR_DONE + ((j - 1) & 1), kPipeBlock);
+        VT_PHL(0);
 #if VT_BULK_COPY
         bulk_tile_out<C>(a, sm.out[0], excl_prev, agg_prev, threadIdx.x - kComputeThreads);
 #else
@@ -313,7 +369,9 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #endif
       }
 #endif
+      VT_PHL(1);
       bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
+      VT_PHL(2);
       const unsigned tile = sm.lb_tile[j & 3];
       if (tile >= a.ntiles) break;
 #if VT_LB_COPY && !VT_BULK_COPY
@@ -334,6 +392,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         }
 #endif
       }
+      VT_PHL(3);
       bar_sync(BAR_AGG + (j & 1), kPipeBlock);
       // (the compute warps already published the aggregate, tile 0 its prefix)
       if (leader && tile != 0 && excl != ~0ull)
@@ -345,6 +404,10 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       }
 #endif
       if (leader) sm.excl[j & 1] = excl;
+      VT_PHL(4);
+#ifdef VT_PHASES
+      if (leader) atomicAdd(&g_phase_lb[7], 1ull);
+#endif
 #if VT_LB_COPY
       excl_prev = excl;
       agg_prev = sm.agg[j & 1];
@@ -364,10 +427,17 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #endif
   } else {
     // compute warps
+    constexpr bool kPF = VT_PREFETCH && C::kPrefetchBytes > 0 && VT_LB_COPY && !VT_BULK_COPY &&
+                         NS == 1 && !VT_GRAB_EARLY && !VT_DEAD_SKIP;
+    unsigned pf_parity = 0;  // phase of the prefetch barrier the next prefetched tile completes
     if (threadIdx.x == 0) {
       const unsigned t = grab_tile(a, C::kTileElems);
       sm.tile = t;
       sm.lb_tile[0] = t;
+      if (kPF) {
+        mbar_init(&sm.mbar, 1);
+        sm.pf_tile = kSentinel;
+      }
     }
     bar_arrive(BAR_GRAB, kPipeBlock);
     unsigned j = 0, prev_agg = 0;
@@ -407,7 +477,14 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       const unsigned long long err_seen = threadIdx.x == 0 ? load_relaxed(&a.ctl->err) : 0ull;
       typename C::TileCount tc;
       unsigned off, agg;
-      C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg);
+      // (prefetched: the tile's bytes are in, or on their way into, sm.in)
+      const bool pf = kPF && sm.pf_tile == tile;
+      if (pf) {
+        mbar_wait(&sm.mbar, pf_parity);
+        pf_parity ^= 1u;
+      }
+      C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg,
+                                                            pf ? sm.in : nullptr);
 #ifdef VT_TRACE
       bool tr_err_tile = false;
       if (threadIdx.x == 0) {
@@ -422,12 +499,15 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
         sm.agg[j & 1] = agg;
       }
+      unsigned grabbed = 0;
+      // prefetch: the next tile is taken now; the atomic's round trip overlaps
+      // the wait for the staging buffer
+      if (kPF) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
       bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
       VT_PH(1);
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase_sub[3], (unsigned long long)ph_t);
 #endif
-      unsigned grabbed = 0;
       bool dead = false;
       const bool early = VT_GRAB_EARLY && NS == 1 && j > 0;
       if (VT_DEAD_SKIP && threadIdx.x == 0) sm.err_now = err_seen;
@@ -491,8 +571,22 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       //   UTF-8 -> UTF-16 at the end of the decode (after 12-15: +0.1-0.4 %,
       //   after 4 / 8: +0.9 %, before: +1.7 %)
       auto grab = [&]() {
-        if (!early) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
+        if (!early && !kPF) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
       };
+      if (kPF && threadIdx.x == 0) {
+        // the next tile's id is here (or nearly): publish it for the loop top
+        // (every compute thread has read sm.tile: they all passed the scan's
+        // barriers) and start its input copy; all words of this tile are in
+        // registers, so the buffer is free
+        unsigned t = grabbed;
+        if (t < a.ntiles && err_seen != kNoError && (err_seen + a.head) / C::kTileElems < t) t = a.ntiles;
+        const bool fetch = C::prefetchable(a, t);
+        if (fetch) fence_proxy_async_smem();  // (the buffer's readers are behind the scan's barriers)
+        if (fetch) bulk_load(sm.in, C::prefetch_src(a, t), C::kPrefetchBytes, &sm.mbar);
+        sm.pf_tile = fetch ? t : kSentinel;
+        sm.tile = t;
+        sm.lb_tile[(j + 1) & 3] = t;
+      }
 #ifndef VT_EXP_NOEMIT
       if (dead || (VT_DEAD_SKIP && NS == 1 && j > 0 && sm.dead))
         grab();
@@ -513,7 +607,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #ifdef VT_TRACE
       if (tr_err_tile) VT_TR_MAX(3);
 #endif
-      if (threadIdx.x == 0 && !early) {
+      if (threadIdx.x == 0 && !early && !kPF) {
         // (the error word was read at the top of the tile: one round trip
         // less on the path every warp waits for at the loop-top barrier)
         unsigned t = grabbed;

@@ -19,10 +19,10 @@ for spec in (sys.argv[1:] or ["2", "3"]):
         run = lambda: vt.utf8_to_utf16_device(d, n, o, d_res=res)
     for _ in range(3): run()
     torch.cuda.synchronize()
-    b0 = np.zeros(12, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b0.ctypes.data)
+    b0 = np.zeros(20, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b0.ctypes.data)
     for _ in range(5): run()
     torch.cuda.synchronize()
-    b = np.zeros(12, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b.ctypes.data)
+    b = np.zeros(20, dtype=np.uint64); L.vt_debug_phases(int(cfg == 3), b.ctypes.data)
     b = (b - b0).astype(np.float64); t = b[7]
     tot = b[:7].sum() / t
     sub = ""
@@ -31,4 +31,9 @@ for spec in (sys.argv[1:] or ["2", "3"]):
     print(sub)
     print(f"cfg{cfg}: cycles per tile (warp 0) total {tot:.0f}: " +
           ", ".join(f"{nm} {b[i] / t:.0f}" for i, nm in enumerate(names)))
+    tl = b[19]
+    if tl > 0:
+        lbn = ["wait-staged", "copy-out", "wait-tile-id", "look-back", "wait-agg+publish"]
+        print(f"cfg{cfg}: look-back warp cycles per tile total {b[12:17].sum() / tl:.0f}: " +
+              ", ".join(f"{nm} {b[12 + i] / tl:.0f}" for i, nm in enumerate(lbn)))
     del d, o
