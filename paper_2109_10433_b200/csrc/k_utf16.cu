@@ -246,7 +246,7 @@ __device__ __forceinline__ Class16 classify16(const Words16& W) {
 template <bool kTranscode, int NT, class Sync, bool kBE = false>
 __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, unsigned* red,
                                              unsigned* scan, TileCount16& tc, unsigned& off,
-                                             unsigned& agg) {
+                                             unsigned& agg, unsigned long long* early = nullptr) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K16_TILE;
   // interior tiles (all but the first and the last one or two): one uniform
@@ -289,6 +289,9 @@ __device__ __forceinline__ void count_tile16(const U16Args& a, unsigned tile, un
     // (end tiles: the zeros outside the input counted as one ASCII unit each)
     tc.cnt = (kTranscode ? c.bytes : c.chars) - (K16_UPT - (hi - tc.lo));
     unsigned total;
+    if (early)
+      publish_total_early<NT>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), early, &a.status[tile],
+                              tile == 0 ? kFlagPre : kFlagAgg, a.epoch, kErrShift);
 #if VT_SCAN1
     off = block_excl_scan1<NT, Sync>(my_err == kNone16 ? tc.cnt : (1u << kErrShift), scan, total);
 #else
@@ -365,8 +368,9 @@ struct Utf16Codec {
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
-                                               unsigned& agg, const uint8_t* = nullptr) {
-    count_tile16<kTranscode, NT, Sync, kBE>(a, tile, red, scan, tc, off, agg);
+                                               unsigned& agg, const uint8_t* = nullptr,
+                                               unsigned long long* early = nullptr) {
+    count_tile16<kTranscode, NT, Sync, kBE>(a, tile, red, scan, tc, off, agg, early);
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,

@@ -567,7 +567,8 @@ struct TileCount {
 template <bool kTranscode, int NT, class Sync, bool kNV = false>
 __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsigned* red,
                                            unsigned* scan, TileCount& tc, unsigned& off,
-                                           unsigned& agg, const uint8_t* pf = nullptr) {
+                                           unsigned& agg, const uint8_t* pf = nullptr,
+                                           unsigned long long* early = nullptr) {
   const unsigned lane = threadIdx.x & 31;
   const long long vt0 = (long long)tile * K8_TILE;  // virtual start of the tile
   // interior: the tile and both halo words lie inside the input.  head < 16, so
@@ -636,6 +637,9 @@ __device__ __forceinline__ void count_tile(const U8Args& a, unsigned tile, unsig
     // (end tiles: the zeros outside the input counted as one ASCII character each)
     tc.cnt = (kTranscode ? co.units : co.chars) - (K8_BPT - (hi - tc.lo));
     unsigned total;
+    if (early)
+      publish_total_early<NT>(my_err == kNone ? tc.cnt : (1u << kErrShift), early, &a.status[tile],
+                              tile == 0 ? kFlagPre : kFlagAgg, a.epoch, kErrShift);
 #if VT_SCAN1
     off = block_excl_scan1<NT, Sync>(my_err == kNone ? tc.cnt : (1u << kErrShift), scan, total);
 #else
@@ -778,8 +782,9 @@ struct Utf8Codec {
   template <bool kTranscode, int NT, class Sync>
   __device__ __forceinline__ static void count(const Args& a, unsigned tile, unsigned* red,
                                                unsigned* scan, TileCount& tc, unsigned& off,
-                                               unsigned& agg, const uint8_t* pf = nullptr) {
-    count_tile<kTranscode, NT, Sync, kNV>(a, tile, red, scan, tc, off, agg, pf);
+                                               unsigned& agg, const uint8_t* pf = nullptr,
+                                               unsigned long long* early = nullptr) {
+    count_tile<kTranscode, NT, Sync, kNV>(a, tile, red, scan, tc, off, agg, pf, early);
   }
   template <class Mid>
   __device__ __forceinline__ static void emit(const Args& a, const TileCount& tc, uint8_t* stage,

@@ -75,7 +75,7 @@ extern __shared__ __align__(16) uint8_t vt_dyn_smem[];
 #ifndef VT_COMPUTE_THREADS
 #define VT_COMPUTE_THREADS 256
 #endif
-constexpr unsigned kPipeTail = 8 * (VT_COMPUTE_THREADS / 32) + 56;
+constexpr unsigned kPipeTail = 8 * (VT_COMPUTE_THREADS / 32) + 64;
 
 static __device__ __noinline__ void vt_check_fail(const char* what, unsigned long long a,
                                                   unsigned long long b, unsigned long long lo,
@@ -501,6 +501,33 @@ __device__ __forceinline__ unsigned scan_step_up(unsigned x, int o) {
       : "+r"(x)
       : "r"(o));
   return x;
+}
+
+// VT_EARLY_PUB: a tile's aggregate goes out before the block scan, not behind
+// its two barriers.  Every warp adds its sum (one REDUX) to a shared 64-bit
+// word (sum in the low half, arrivals in the high half); the warp that arrives
+// last has the tile's total and stores the status word at once, unless the
+// total carries an error count (bits kErrShift and up: those tiles publish
+// their clipped count later, as before).  Every tile taken after this one
+// waits for this store in its look-back, so each cycle it comes earlier is a
+// cycle off their copy-out.  The last warp also re-arms the word: the others
+// are held by the scan's barrier until it gets there.
+#ifndef VT_EARLY_PUB
+#define VT_EARLY_PUB 0
+#endif
+template <int THREADS>
+__device__ __forceinline__ void publish_total_early(unsigned v, unsigned long long* word,
+                                                    unsigned long long* status, unsigned long long flag,
+                                                    unsigned epoch, int err_shift) {
+  const unsigned s = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long old = atomicAdd(word, (1ull << 32) | s);
+    if ((unsigned)(old >> 32) == THREADS / 32 - 1) {
+      const unsigned total = (unsigned)old + s;
+      *word = 0;
+      if ((total >> err_shift) == 0) store_status(status, pack_status(flag, epoch, total));
+    }
+  }
 }
 
 // Block-wide exclusive scan of one unsigned per thread (THREADS threads).

@@ -164,13 +164,14 @@ struct PipeSmem {
   // by the CTA-local tile number, guarded by the named barriers below)
   unsigned lb_tile[4], agg[2];
   unsigned long long excl[2];
+  unsigned long long early;  // publish_total_early's sum / arrival word
 };
 
 // (vt_device.cuh's staging-store check assumes this tail size)
 struct PipeTailProbe {
   static constexpr int kStageBytes = 16, kNStage = 1, kPrefetchBytes = 0;
 };
-static_assert(offsetof(PipeSmem<PipeTailProbe>, excl) + 16 - offsetof(PipeSmem<PipeTailProbe>, scan) ==
+static_assert(offsetof(PipeSmem<PipeTailProbe>, early) + 8 - offsetof(PipeSmem<PipeTailProbe>, scan) ==
                   kPipeTail,
               "PipeSmem tail");
 
@@ -438,6 +439,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         mbar_init(&sm.mbar, 1);
         sm.pf_tile = kSentinel;
       }
+      sm.early = 0;
     }
     bar_arrive(BAR_GRAB, kPipeBlock);
     unsigned j = 0, prev_agg = 0;
@@ -484,7 +486,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         pf_parity ^= 1u;
       }
       C::template count<true, kComputeThreads, ComputeSync>(a, tile, sm.red, sm.scan, tc, off, agg,
-                                                            pf ? sm.in : nullptr);
+                                                            pf ? sm.in : nullptr, VT_EARLY_PUB ? &sm.early : nullptr);
 #ifdef VT_TRACE
       bool tr_err_tile = false;
       if (threadIdx.x == 0) {
@@ -496,7 +498,10 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       if (threadIdx.x == 0) {
         // publish the aggregate right away (tile 0: the inclusive prefix), so
         // other CTAs' look-backs never wait on this CTA's look-back warp
-        store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
+        // (with VT_EARLY_PUB the last warp through the count did it already,
+        // except for tiles with an error or an end of the input in them)
+        if (!(VT_EARLY_PUB && tc.simple))
+          store_status(&a.status[tile], pack_status(tile == 0 ? kFlagPre : kFlagAgg, a.epoch, agg));
         sm.agg[j & 1] = agg;
       }
       unsigned grabbed = 0;
