@@ -958,6 +958,11 @@ static int set_smem_attr() {
     const int rc = (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    sizeof(PipeSmem<Utf8Codec<false>>));
     if (rc) return rc;
+#ifdef VT_CARVEOUT
+    // (A/B: preferred shared-memory carveout in percent; more than 4 CTAs per SM
+    // need more shared memory than the driver's default choice provides)
+    if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, VT_CARVEOUT)) return 1;
+#endif
   }
   return 0;
 }

@@ -468,6 +468,59 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// Barrier BASE + (sel mod N) with the id as an immediate (N = 2 or 4; a uniform
+// branch picks it).  With an id in a register ptxas cannot tell which barriers
+// a kernel uses and books all 16 ("used 16 barriers"), and an SM hands out 64:
+// that alone capped the transcode kernels at 4 CTAs per SM whatever their
+// registers and shared memory (cudaOccupancyMaxActiveBlocksPerMultiprocessor
+// said 4 for a 192-thread, 40-register, 20 KiB variant).
+template <int ID, int NT>
+__device__ __forceinline__ void bar_sync_imm() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NT) : "memory");
+}
+template <int ID, int NT>
+__device__ __forceinline__ void bar_arrive_imm() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(NT) : "memory");
+}
+// (VT_BAR_IMM=0, the default: the id stays in a register -- with 56 registers
+// per thread the register file caps the kernels at 4 CTAs per SM anyway, and
+// the uniform branches cost ~0.5 %.  Shapes with more CTAs per SM need 1; none
+// of them was faster, profiles/r02/ab_r3w_occupancy_shapes.txt.)
+#ifndef VT_BAR_IMM
+#define VT_BAR_IMM 0
+#endif
+template <int BASE, int N, int NT>
+__device__ __forceinline__ void bar_sync_sel(unsigned sel) {
+  static_assert(N == 2 || N == 4, "two or four ids");
+  sel &= N - 1;
+  if (!VT_BAR_IMM) {
+    bar_sync(BASE + (int)sel, NT);
+    return;
+  }
+  if (N == 4 && sel >= 2) {
+    if (sel == 3) bar_sync_imm<BASE + (N == 4 ? 3 : 1), NT>();
+    else bar_sync_imm<BASE + (N == 4 ? 2 : 0), NT>();
+  } else {
+    if (sel == 1) bar_sync_imm<BASE + 1, NT>();
+    else bar_sync_imm<BASE, NT>();
+  }
+}
+template <int BASE, int N, int NT>
+__device__ __forceinline__ void bar_arrive_sel(unsigned sel) {
+  static_assert(N == 2 || N == 4, "two or four ids");
+  sel &= N - 1;
+  if (!VT_BAR_IMM) {
+    bar_arrive(BASE + (int)sel, NT);
+    return;
+  }
+  if (N == 4 && sel >= 2) {
+    if (sel == 3) bar_arrive_imm<BASE + (N == 4 ? 3 : 1), NT>();
+    else bar_arrive_imm<BASE + (N == 4 ? 2 : 0), NT>();
+  } else {
+    if (sel == 1) bar_arrive_imm<BASE + 1, NT>();
+    else bar_arrive_imm<BASE, NT>();
+  }
+}
 
 // ---- row bookkeeping of the barrier-free validate kernels --------------------
 // Warp gw takes rows gw, gw + nwarps, ... and stores, per row, its running

@@ -308,6 +308,8 @@ __device__ __forceinline__ void bulk_tile_out(const typename C::Args& a, const u
 //     ids per kind are not enough for GRAB with two buffers, where GRAB(j+2)
 //     is arrived at while the look-back warp may still be before GRAB(j+1).
 constexpr int BAR_EXCL = 2, BAR_AGG = 4, BAR_GRAB = 8, BAR_DONE = 6;
+// (ids as immediates, see bar_sync_sel: the kernel then books 10 or 12 barriers,
+// not 16)
 
 #ifdef VT_PHASES
 // per-phase cycle totals of warp 0 of every CTA (perf probe): loop-top sync,
@@ -344,6 +346,15 @@ template <class C>
 __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSmem<C>& sm) {
   constexpr int NS = C::kNStage;
   static_assert(NS == 1 || NS == 2, "one or two staging buffers");
+  // GRAB ids: four in general (see above); with one staging buffer and the
+  // plain grab two are enough -- GRAB(j+2) is arrived at after the compute warps
+  // waited for EXCL(j), which the look-back warp arrives at after its wait on
+  // GRAB(j+1), so GRAB(j) is complete
+#ifdef VT_GRAB_IDS
+  constexpr int kGrabIds = VT_GRAB_IDS;
+#else
+  constexpr int kGrabIds = (NS == 1 && !VT_GRAB_EARLY && VT_LB_COPY) ? 2 : 4;
+#endif
   if (threadIdx.x == 0) VT_TR_MIN(0);
   if (threadIdx.x >= kComputeThreads) {
     const bool leader = threadIdx.x == kComputeThreads;
@@ -361,7 +372,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // offset was resolved in the previous round: copy it out, then hand the
       // buffer back (EXCL(j-1) = "copy done")
       if (j > 0) {
-        bar_sync(BAR_DONE + ((j - 1) & 1), kPipeBlock);
+        bar_sync_sel<BAR_DONE, 2, kPipeBlock>((j - 1));
         VT_PHL(0);
 #if VT_BULK_COPY
         bulk_tile_out<C>(a, sm.out[0], excl_prev, agg_prev, threadIdx.x - kComputeThreads);
@@ -371,14 +382,14 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       }
 #endif
       VT_PHL(1);
-      bar_sync(BAR_GRAB + (j & 3), kPipeBlock);
+      bar_sync_sel<BAR_GRAB, kGrabIds, kPipeBlock>(j);
       VT_PHL(2);
       const unsigned tile = sm.lb_tile[j & 3];
       if (tile >= a.ntiles) break;
 #if VT_LB_COPY && !VT_BULK_COPY
       // (the compute warps wait for the buffer only after counting tile j; after
       // the CTA's last tile nobody waits, so the arrival comes behind the break)
-      if (j > 0) bar_arrive(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
+      if (j > 0) bar_arrive_sel<BAR_EXCL, 2, kPipeBlock>((j - 1));
 #endif
       unsigned long long excl = 0;
       if (tile != 0) {
@@ -394,7 +405,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #endif
       }
       VT_PHL(3);
-      bar_sync(BAR_AGG + (j & 1), kPipeBlock);
+      bar_sync_sel<BAR_AGG, 2, kPipeBlock>(j);
       // (the compute warps already published the aggregate, tile 0 its prefix)
       if (leader && tile != 0 && excl != ~0ull)
         store_status(&a.status[tile], pack_status(kFlagPre, a.epoch, excl + sm.agg[j & 1]));
@@ -417,10 +428,10 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // j-1 (in flight during this look-back) has read the staging buffer
       if (leader) bulk_wait_read();
       __syncwarp();
-      bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
+      bar_arrive_sel<BAR_EXCL, 2, kPipeBlock>(j);
 #endif
 #else
-      bar_arrive(BAR_EXCL + (j & 1), kPipeBlock);
+      bar_arrive_sel<BAR_EXCL, 2, kPipeBlock>(j);
 #endif
     }
 #if VT_LB_COPY && VT_BULK_COPY
@@ -441,7 +452,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       }
       sm.early = 0;
     }
-    bar_arrive(BAR_GRAB, kPipeBlock);
+    bar_arrive_imm<BAR_GRAB, kPipeBlock>();
     unsigned j = 0, prev_agg = 0;
 #ifdef VT_PHASES
     long long ph_t = clock64();
@@ -451,7 +462,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #ifdef VT_PROBE
       const long long t0 = clock64();
 #endif
-      bar_sync(BAR_EXCL + ((j - 1) & 1), kPipeBlock);
+      bar_sync_sel<BAR_EXCL, 2, kPipeBlock>((j - 1));
       VT_PH(2);
 #ifdef VT_PROBE
       if (threadIdx.x == 0) {
@@ -508,7 +519,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       // prefetch: the next tile is taken now; the atomic's round trip overlaps
       // the wait for the staging buffer
       if (kPF) atom_inc_pinned(&a.ctl->tile_counter, threadIdx.x == 0, grabbed);
-      bar_arrive(BAR_AGG + (j & 1), kPipeBlock);
+      bar_arrive_sel<BAR_AGG, 2, kPipeBlock>(j);
       VT_PH(1);
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase_sub[3], (unsigned long long)ph_t);
@@ -520,7 +531,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
       static_assert(NS == 1 && !VT_GRAB_EARLY && !VT_DEAD_SKIP, "bulk copy-out: one buffer, plain grab");
       // tile j's own offset (the staging phase) and the buffer, both from the
       // look-back warp
-      bar_sync(BAR_EXCL + (j & 1), kPipeBlock);
+      bar_sync_sel<BAR_EXCL, 2, kPipeBlock>(j);
       VT_PH(2);
       VT_PH(3);
       VT_PH(4);
@@ -567,7 +578,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
           dead = true;
           agg = 0;
         }
-        if (early && VT_GRAB_EARLY == 2) bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
+        if (early && VT_GRAB_EARLY == 2) bar_arrive_sel<BAR_GRAB, kGrabIds, kPipeBlock>((j + 1));
       }
       // thread 0 takes the next tile from inside the decode (the codec says
       // where: Codec::emit calls `grab`); measured per codec, ms/GiB:
@@ -606,7 +617,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
 #if VT_BULK_COPY
       fence_proxy_async_smem();
 #endif
-      bar_arrive(BAR_DONE + (j & 1), kPipeBlock);
+      bar_arrive_sel<BAR_DONE, 2, kPipeBlock>(j);
 #endif
       VT_PH(5);
 #ifdef VT_TRACE
@@ -621,7 +632,7 @@ __device__ __forceinline__ void transcode_body(const typename C::Args& a, PipeSm
         sm.tile = t;
         sm.lb_tile[(j + 1) & 3] = t;
       }
-      if (!(early && VT_GRAB_EARLY == 2)) bar_arrive(BAR_GRAB + ((j + 1) & 3), kPipeBlock);
+      if (!(early && VT_GRAB_EARLY == 2)) bar_arrive_sel<BAR_GRAB, kGrabIds, kPipeBlock>((j + 1));
       VT_PH(6);
 #ifdef VT_PHASES
       if (threadIdx.x == 0) atomicAdd(&g_phase[7], 1ull);
